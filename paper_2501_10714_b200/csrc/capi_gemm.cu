@@ -1,0 +1,130 @@
+// capi_gemm.cu — extern "C" error plumbing + expert-FFN GEMM entry points.
+#include <cstdio>
+#include <string>
+
+#include "capi_common.h"
+#include "gemm.h"
+
+namespace fsmoe {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+int config_error(const std::string& msg) {
+  g_last_error = msg;
+  return FSMOE_CONFIG_ERROR;
+}
+
+int invariant_error(const std::string& msg) {
+  g_last_error = msg;
+  return FSMOE_INVARIANT_ERROR;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return FSMOE_OK;
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return FSMOE_CUDA_ERROR;
+}
+
+namespace {
+
+__global__ void act_f32_kernel(int op, long long rows, int units, const float* __restrict__ in,
+                               const float* __restrict__ z, float* __restrict__ out,
+                               float* __restrict__ out2) {
+  long long n = rows * units;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long r = i / units;
+    int u = static_cast<int>(i - r * units);
+    int gcol = (u / 128) * 256 + (u % 128);  // interleaved gate/up column of unit u
+    switch (op) {
+      case 2: {  // gelu fwd: in = Z (rows x units) -> out = gelu(Z)
+        float v = in[i];
+        out[i] = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+        break;
+      }
+      case 3: {  // swiglu fwd: in = Z (rows x 2*units interleaved) -> out = H
+        const float* zr = in + r * 2LL * units;
+        float g = zr[gcol], up = zr[gcol + 128];
+        out[i] = g / (1.0f + expf(-g)) * up;
+        break;
+      }
+      case 4: {  // gelu bwd: in = dH, z = Z -> out = dZ
+        float v = z[i];
+        float cdf = 0.5f * (1.0f + erff(v * 0.70710678118654752f));
+        float pdf = 0.39894228040143268f * expf(-0.5f * v * v);
+        out[i] = in[i] * (cdf + v * pdf);
+        break;
+      }
+      case 5: {  // swiglu bwd: in = dH (rows x units), z = Z interleaved -> out = dZ interleaved
+        const float* zr = z + r * 2LL * units;
+        float* dr = out + r * 2LL * units;
+        float g = zr[gcol], up = zr[gcol + 128];
+        float sg = 1.0f / (1.0f + expf(-g));
+        float dh = in[i];
+        dr[gcol] = dh * up * sg * (1.0f + g * (1.0f - sg));
+        dr[gcol + 128] = dh * g * sg;
+        break;
+      }
+      default:
+        break;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace fsmoe
+
+extern "C" {
+
+const char* fsmoe_last_error(void) { return fsmoe::g_last_error.c_str(); }
+
+int fsmoe_abi_version(void) { return 1; }
+
+int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
+  using namespace fsmoe;
+  if (!d) return config_error("gemm: null descriptor");
+  GemmProblem p;
+  p.kind = d->kind == 1 ? GemmKind::KGrouped : GemmKind::RowGrouped;
+  p.nblk = d->nblk;
+  p.rows = d->rows;
+  p.K = d->K;
+  p.N = d->N;
+  p.Mo = d->Mo;
+  p.No = d->No;
+  p.n_w = d->n_w;
+  p.b_mn_major = d->b_mn_major != 0;
+  p.A = d->A;
+  p.B = d->B;
+  p.valid_rows = d->valid_rows;
+  p.epi = static_cast<Epi>(d->epi);
+  p.D = d->D;
+  p.D2 = d->D2;
+  p.Zin = d->Zin;
+  p.ldd = d->ldd;
+  p.ldd2 = d->ldd2;
+  p.ldz = d->ldz;
+  p.accumulate = d->accumulate != 0;
+  if (d->epi < 0 || d->epi > 5) return config_error("gemm: unknown epilogue");
+  if (p.kind == GemmKind::KGrouped && p.epi != Epi::StoreF32)
+    return config_error("gemm: k-grouped (wgrad) problems take the f32 store epilogue");
+  int rc = d->precision == 1 ? gemm_simt_launch(p, as_stream(stream))
+                             : gemm_sm100_launch(p, as_stream(stream));
+  if (rc == cudaErrorInvalidValue) return config_error("gemm: unsupported problem shape");
+  return cuda_status(static_cast<cudaError_t>(rc), "fsmoe_grouped_gemm");
+}
+
+int fsmoe_activation_f32(int op, long long rows, int units, const float* in, const float* z,
+                         float* out, float* out2, void* stream) {
+  using namespace fsmoe;
+  if (op < 2 || op > 5) return config_error("activation: unknown op");
+  if (rows <= 0 || units <= 0) return FSMOE_OK;
+  if ((op == 3 || op == 5) && units % 128) return config_error("activation: swiglu units % 128");
+  long long n = rows * units;
+  int grid = static_cast<int>((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  act_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(op, rows, units, in, z, out, out2);
+  return cuda_status(cudaGetLastError(), "fsmoe_activation_f32");
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// gemm.h — grouped expert GEMM problem description shared by the tcgen05
+// kernel (bf16, gemm_sm100.cu) and the fp32 SIMT check-mode kernel
+// (gemm_simt.cu). Host-side only types plus the launch entry points.
+//
+// Two problem shapes cover the whole expert FFN forward and backward
+// (SURVEY.md Appendix D):
+//
+//  ROW-GROUPED (forward, dgrad):   D[b] (rows x N) = A[b] (rows x K) . B[w(b)] (K x N)
+//    A: [nblk][rows][K] row-major (K contiguous)           -> K-major operand
+//    B: K-major   [E_w][N][K]  (forward weights)
+//       MN-major  [E_w][K][N]  (dgrad: the forward weight read transposed)
+//    w(b) = b % E_w ; D: [nblk][rows][N]
+//
+//  K-GROUPED (wgrad):   D[e] (Mo x No) = sum_{b : b % E_w == e} A[b]^T . B[b]
+//    A: [nblk][rows][Mo] (Mo contiguous) -> MN-major operand
+//    B: [nblk][rows][No] (No contiguous) -> MN-major operand
+//    D: [E_w][Mo][No] fp32, optionally accumulated (pipeline chunks).
+//
+// `valid_rows[b]` (optional, device int64 per block) is the dispatch fill of
+// that block: row tiles entirely past it are skipped (their rows are capacity
+// padding) and wgrad's K extent stops at round_up(valid, 64).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fsmoe {
+
+enum class GemmKind : int { RowGrouped = 0, KGrouped = 1 };
+
+enum class Epi : int {
+  StoreBF16 = 0,   // D bf16
+  StoreF32 = 1,    // D fp32 (accumulate when `accumulate`)
+  GeluFwd = 2,     // Z = acc (bf16), H = gelu(acc) (bf16)           N = H
+  SwigluFwd = 3,   // acc cols interleaved [gate128|up128]: Z = acc, H = silu(g)*u
+  GeluBwd = 4,     // acc = dH; dZ = dH * gelu'(Z)                   N = H
+  SwigluBwd = 5,   // acc = dH (N = H); writes dZ at interleaved gate/up columns
+};
+
+struct GemmProblem {
+  GemmKind kind = GemmKind::RowGrouped;
+  int nblk = 0;        // A/B blocks (row-grouped: output blocks too)
+  int rows = 0;        // rows per block
+  int K = 0;           // row-grouped reduction dim
+  int N = 0;           // row-grouped output columns
+  int Mo = 0, No = 0;  // k-grouped output dims
+  int n_w = 1;         // weight (expert) count E_w; w(b) = b % n_w
+  bool b_mn_major = false;  // row-grouped only (k-grouped: both MN-major)
+  const void* A = nullptr;
+  const void* B = nullptr;
+  const long long* valid_rows = nullptr;  // [nblk] or null
+  // epilogue
+  Epi epi = Epi::StoreBF16;
+  void* D = nullptr;         // main output
+  void* D2 = nullptr;        // GeluFwd/SwigluFwd: H output
+  const void* Zin = nullptr; // GeluBwd/SwigluBwd: saved pre-activation
+  long long ldd = 0;         // D row stride (elements)
+  long long ldd2 = 0;        // D2 row stride
+  long long ldz = 0;         // Zin row stride
+  bool accumulate = false;   // StoreF32: D += acc
+};
+
+// bf16 operands, fp32 accumulate in TMEM (tcgen05). Returns cudaError_t.
+int gemm_sm100_launch(const GemmProblem& p, cudaStream_t stream);
+// fp32 operands/outputs, SIMT FFMA; same problem semantics (check mode).
+int gemm_simt_launch(const GemmProblem& p, cudaStream_t stream);
+
+}  // namespace fsmoe

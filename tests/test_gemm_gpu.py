@@ -1,0 +1,195 @@
+"""Grouped expert GEMM (tcgen05 bf16 + fp32 SIMT check mode) vs a torch fp32
+reference of the same op. The reference (FSMoE artifact) has no expert FFN
+(it only counts GEMMs, proj/src/workload.cpp:70), so this is the
+floating-point kernel's "plain PyTorch fp32 reference" check.
+
+Tolerances: bf16 outputs rel 2e-2 of max|ref| (bf16 rounding of inputs and
+outputs, fp32 accumulate); fp32 outputs of bf16 GEMMs rel 5e-3; fp32 check
+mode rel 1e-5.
+"""
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+def _ops():
+    from paper_2501_10714_b200 import ops
+    return ops
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-30)).item()
+
+
+def _rand(*shape, dtype=torch.bfloat16, scale=1.0):
+    return (torch.randn(*shape, device="cuda") * scale).to(dtype)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("nblk,rows,K,N,n_w", [(3, 200, 192, 320, 3), (4, 256, 512, 512, 2),
+                                               (2, 77, 64, 64, 1), (16, 128, 1024, 512, 16)])
+def test_row_grouped_kmajor(precision, nblk, rows, K, N, n_w):
+    ops = _ops()
+    dt = torch.bfloat16 if precision == 0 else torch.float32
+    torch.manual_seed(0)
+    A = _rand(nblk, rows, K, dtype=dt)
+    B = _rand(n_w, N, K, dtype=dt, scale=K ** -0.5)
+    D = torch.empty(nblk, rows, N, device="cuda", dtype=dt)
+    ops.grouped_gemm("row", A, B, D, nblk=nblk, rows=rows, K=K, N=N, n_w=n_w,
+                     epi="store_bf16" if precision == 0 else "store_f32", precision=precision)
+    torch.cuda.synchronize()
+    ref = torch.stack([A[b].double() @ B[b % n_w].double().T for b in range(nblk)])
+    assert _rel(D, ref) < (2e-2 if precision == 0 else 1e-5)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_row_grouped_mnmajor_b(precision):
+    ops = _ops()
+    dt = torch.bfloat16 if precision == 0 else torch.float32
+    nblk, rows, K, N, n_w = 4, 300, 256, 384, 2
+    A = _rand(nblk, rows, K, dtype=dt)
+    B = _rand(n_w, K, N, dtype=dt, scale=K ** -0.5)  # stored [w][K][N]
+    D = torch.empty(nblk, rows, N, device="cuda", dtype=dt)
+    ops.grouped_gemm("row", A, B, D, nblk=nblk, rows=rows, K=K, N=N, n_w=n_w, b_mn_major=True,
+                     epi="store_bf16" if precision == 0 else "store_f32", precision=precision)
+    torch.cuda.synchronize()
+    ref = torch.stack([A[b].double() @ B[b % n_w].double() for b in range(nblk)])
+    assert _rel(D, ref) < (2e-2 if precision == 0 else 1e-5)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_k_grouped_wgrad(precision, accumulate):
+    ops = _ops()
+    dt = torch.bfloat16 if precision == 0 else torch.float32
+    nblk, rows, Mo, No, n_w = 6, 200, 192, 320, 3
+    A = _rand(nblk, rows, Mo, dtype=dt)
+    B = _rand(nblk, rows, No, dtype=dt)
+    D0 = torch.randn(n_w, Mo, No, device="cuda")
+    D = D0.clone()
+    ops.grouped_gemm("k", A, B, D, nblk=nblk, rows=rows, Mo=Mo, No=No, n_w=n_w, epi="store_f32",
+                     accumulate=accumulate, precision=precision)
+    torch.cuda.synchronize()
+    ref = torch.zeros(n_w, Mo, No, dtype=torch.float64, device="cuda")
+    for b in range(nblk):
+        ref[b % n_w] += A[b].double().T @ B[b].double()
+    if accumulate:
+        ref += D0.double()
+    assert _rel(D, ref) < (5e-3 if precision == 0 else 1e-5)
+
+
+def test_valid_rows_skip_and_kextent():
+    ops = _ops()
+    nblk, rows, K, N = 4, 512, 128, 256
+    valid = torch.tensor([0, 100, 512, 300], device="cuda", dtype=torch.int64)
+    A = _rand(nblk, rows, K)
+    for b in range(nblk):
+        A[b, valid[b]:] = 0
+    B = _rand(nblk, N, K, scale=K ** -0.5)
+    D = torch.full((nblk, rows, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    ops.grouped_gemm("row", A, B, D, nblk=nblk, rows=rows, K=K, N=N, n_w=nblk, valid_rows=valid)
+    torch.cuda.synchronize()
+    for b in range(nblk):
+        v = int(valid[b])
+        vr = (v + 127) // 128 * 128  # computed tiles cover whole 128-row tiles
+        ref = A[b, :vr].double() @ B[b].double().T
+        if vr:
+            assert _rel(D[b, :vr], ref) < 2e-2
+        if vr < rows:
+            assert torch.isnan(D[b, vr:].float()).all()  # skipped tiles untouched
+    # wgrad over the same blocks: K extent = valid rows
+    G = _rand(nblk, rows, N)
+    W = torch.zeros(nblk, K, N, device="cuda")
+    ops.grouped_gemm("k", A, G, W, nblk=nblk, rows=rows, Mo=K, No=N, n_w=nblk, epi="store_f32",
+                     valid_rows=valid)
+    torch.cuda.synchronize()
+    for b in range(nblk):
+        v = int(valid[b])
+        ref = A[b, :v].double().T @ G[b, :v].double()
+        if v == 0:
+            assert W[b].abs().max().item() == 0
+        else:
+            assert _rel(W[b], ref) < 5e-3
+
+
+def test_gelu_epilogues():
+    ops = _ops()
+    nblk, rows, K, H = 2, 256, 256, 512
+    X = _rand(nblk, rows, K)
+    W1 = _rand(nblk, H, K, scale=K ** -0.5)
+    Z = torch.empty(nblk, rows, H, device="cuda", dtype=torch.bfloat16)
+    Hh = torch.empty_like(Z)
+    ops.grouped_gemm("row", X, W1, Z, nblk=nblk, rows=rows, K=K, N=H, n_w=nblk, epi="gelu_fwd",
+                     D2=Hh, ldd2=H)
+    torch.cuda.synchronize()
+    zref = torch.stack([X[b].float() @ W1[b].float().T for b in range(nblk)])
+    assert _rel(Z, zref) < 2e-2
+    assert _rel(Hh, F.gelu(Z.float())) < 2e-2
+    # backward epilogue: dZ = (dO . W2^T) * gelu'(Z), W2 stored [w][M][H] (MN-major B)
+    M = 256
+    dO = _rand(nblk, rows, M)
+    W2 = _rand(nblk, M, H, scale=M ** -0.5)
+    dZ = torch.empty(nblk, rows, H, device="cuda", dtype=torch.bfloat16)
+    ops.grouped_gemm("row", dO, W2, dZ, nblk=nblk, rows=rows, K=M, N=H, n_w=nblk, b_mn_major=True,
+                     epi="gelu_bwd", Zin=Z, ldz=H)
+    torch.cuda.synchronize()
+    z = Z.float().requires_grad_(True)
+    g = torch.autograd.grad(F.gelu(z), z, torch.stack([dO[b].float() @ W2[b].float()
+                                                       for b in range(nblk)]))[0]
+    assert _rel(dZ, g) < 2e-2
+
+
+def test_swiglu_epilogues():
+    ops = _ops()
+    nblk, rows, K, H = 2, 256, 256, 256
+    X = _rand(nblk, rows, K)
+    W1 = _rand(nblk, 2 * H, K, scale=K ** -0.5)  # interleaved [gate128 | up128] blocks
+    Z = torch.empty(nblk, rows, 2 * H, device="cuda", dtype=torch.bfloat16)
+    Hh = torch.empty(nblk, rows, H, device="cuda", dtype=torch.bfloat16)
+    ops.grouped_gemm("row", X, W1, Z, nblk=nblk, rows=rows, K=K, N=2 * H, n_w=nblk,
+                     epi="swiglu_fwd", D2=Hh, ldd2=H)
+    torch.cuda.synchronize()
+    zref = torch.stack([X[b].float() @ W1[b].float().T for b in range(nblk)])
+    assert _rel(Z, zref) < 2e-2
+    zb = Z.float().view(nblk, rows, H // 128, 2, 128)
+    g, u = zb[:, :, :, 0, :].reshape(nblk, rows, H), zb[:, :, :, 1, :].reshape(nblk, rows, H)
+    assert _rel(Hh, F.silu(g) * u) < 2e-2
+    M = 256
+    dO = _rand(nblk, rows, M)
+    W2 = _rand(nblk, M, H, scale=M ** -0.5)
+    dZ = torch.empty(nblk, rows, 2 * H, device="cuda", dtype=torch.bfloat16)
+    ops.grouped_gemm("row", dO, W2, dZ, nblk=nblk, rows=rows, K=M, N=H, n_w=nblk, b_mn_major=True,
+                     epi="swiglu_bwd", Zin=Z, ldz=2 * H, ldd=2 * H)
+    torch.cuda.synchronize()
+    gg, uu = g.clone().requires_grad_(True), u.clone().requires_grad_(True)
+    dH = torch.stack([dO[b].float() @ W2[b].float() for b in range(nblk)])
+    dg, du = torch.autograd.grad(F.silu(gg) * uu, (gg, uu), dH)
+    dzb = dZ.float().view(nblk, rows, H // 128, 2, 128)
+    assert _rel(dzb[:, :, :, 0, :].reshape(nblk, rows, H), dg) < 2e-2
+    assert _rel(dzb[:, :, :, 1, :].reshape(nblk, rows, H), du) < 2e-2
+
+
+def test_large_perf_smoke():
+    """One C2-shaped forward GEMM; also reports achieved TFLOP/s."""
+    ops = _ops()
+    E, C, M, H = 16, 1024, 1024, 4096
+    X = _rand(E, C, M)
+    W1 = _rand(E, H, M, scale=M ** -0.5)
+    Z = torch.empty(E, C, H, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        ops.grouped_gemm("row", X, W1, Z, nblk=E, rows=C, K=M, N=H, n_w=E)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    n = 10
+    for _ in range(n):
+        ops.grouped_gemm("row", X, W1, Z, nblk=E, rows=C, K=M, N=H, n_w=E)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / n
+    tflops = 2 * E * C * M * H / ms / 1e9
+    print(f"\n[gemm] E{E} C{C} M{M} H{H}: {ms*1e3:.1f} us  {tflops:.0f} TFLOP/s")
+    ref = X[3].float() @ W1[3].float().T
+    assert _rel(Z[3], ref) < 2e-2
