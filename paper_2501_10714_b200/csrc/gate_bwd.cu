@@ -1,0 +1,318 @@
+// gate_bwd.cu — backward of the gate (the reference has none, SPEC.md:12;
+// semantics of SURVEY.md Appendix D):
+//   d_weight -> d scores:  softmax over the kept set (noisy / cosine / EC),
+//                          logistic (sigmoid); dropped picks have d_weight 0 but
+//                          still couple through the softmax normaliser.
+//   d scores -> params:    dW = x^T dS (fp64, deterministic split-T reduction),
+//                          dx += dS W^T; noisy adds the softplus(x W_noise)*n
+//                          branch; cosine goes through q = P x and the norms.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "capi_common.h"
+#include "kernels.h"
+#include "route_common.cuh"
+
+namespace fsmoe {
+namespace {
+
+using namespace fsmoe_dev;
+
+// dS for token-choice gates (T x E, dense, zero elsewhere).
+// kind 0/2: softmax over the k kept picks; kind 1: sigmoid.
+__global__ void dscore_token_kernel(int kind, int T, int E, int k, const int* __restrict__ pexp,
+                                    const double* __restrict__ pw, const double* __restrict__ dw,
+                                    double* __restrict__ dS) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  double* row = dS + static_cast<long long>(t) * E;
+  for (int e = 0; e < E; ++e) row[e] = 0.0;
+  const long long b = static_cast<long long>(t) * k;
+  if (kind == 1) {
+    for (int j = 0; j < k; ++j) {
+      double w = pw[b + j];
+      row[pexp[b + j]] = dw[b + j] * w * (1.0 - w);
+    }
+    return;
+  }
+  double sig = 0.0;
+  for (int j = 0; j < k; ++j) sig += pw[b + j] * dw[b + j];
+  for (int j = 0; j < k; ++j) row[pexp[b + j]] = pw[b + j] * (dw[b + j] - sig);
+}
+
+// dS for expert choice, layout E x T (like the forward scores).
+__global__ void dscore_ec_kernel(int T, int E, int C, const int* __restrict__ ptok,
+                                 const double* __restrict__ pw, const double* __restrict__ dw,
+                                 double* __restrict__ dS) {
+  __shared__ double red[32];
+  const int e = blockIdx.x;
+  const long long b = static_cast<long long>(e) * C;
+  double part = 0.0;
+  for (int j = threadIdx.x; j < C; j += blockDim.x) part += pw[b + j] * dw[b + j];
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  double sig = 0.0;
+  for (int i = 0; i < static_cast<int>(blockDim.x) / 32; ++i) sig += red[i];
+  double* row = dS + static_cast<long long>(e) * T;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) row[t] = 0.0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < C; j += blockDim.x) row[ptok[b + j]] = pw[b + j] * (dw[b + j] - sig);
+}
+
+// noisy: dZ = dS * n * sigmoid(spread)
+__global__ void noisy_dz_kernel(long long n, const double* __restrict__ dS,
+                                const double* __restrict__ noise, const double* __restrict__ spread,
+                                double* __restrict__ dZ) {
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < n) dZ[i] = dS[i] * noise[i] / (1.0 + exp(-spread[i]));
+}
+
+// cosine, per token: dq[t] = sum_e dS[t][e] (w_e/(|q||w_e|) - s_e q/|q|^2);
+// qn[t] = q/|q|.
+__global__ void cosine_dq_kernel(int T, int E, int P, const double* __restrict__ q,
+                                 const double* __restrict__ w, const double* __restrict__ enorm,
+                                 const double* __restrict__ s, const double* __restrict__ dS,
+                                 double* __restrict__ dq, double* __restrict__ qn) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const double* qt = q + static_cast<long long>(t) * P;
+  double pn = 0.0;
+  for (int p = 0; p < P; ++p) pn += qt[p] * qt[p];
+  const double qnorm = sqrt(pn);
+  double* d = dq + static_cast<long long>(t) * P;
+  for (int p = 0; p < P; ++p) {
+    d[p] = 0.0;
+    qn[static_cast<long long>(t) * P + p] = qt[p] / qnorm;
+  }
+  for (int e = 0; e < E; ++e) {
+    double g = dS[static_cast<long long>(t) * E + e];
+    if (g == 0.0) continue;
+    double wn = sqrt(enorm[e]);
+    double se = s[static_cast<long long>(t) * E + e];
+    for (int p = 0; p < P; ++p)
+      d[p] += g * (w[static_cast<long long>(p) * E + e] / (qnorm * wn) - se * qt[p] / pn);
+  }
+}
+
+// b[e] = sum_t dS[t][e] * s[t][e]
+__global__ void cosine_b_kernel(int T, int E, const double* __restrict__ s,
+                                const double* __restrict__ dS, double* __restrict__ b) {
+  __shared__ double red[32];
+  const int e = blockIdx.x;
+  double part = 0.0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x)
+    part += dS[static_cast<long long>(t) * E + e] * s[static_cast<long long>(t) * E + e];
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int i = 0; i < static_cast<int>(blockDim.x) / 32; ++i) acc += red[i];
+    b[e] = acc;
+  }
+}
+
+// dW[p][e] += A[p][e]/|w_e| - w[p][e] b[e]/|w_e|^2
+__global__ void cosine_dw_kernel(int P, int E, const double* __restrict__ A,
+                                 const double* __restrict__ w, const double* __restrict__ enorm,
+                                 const double* __restrict__ b, double* __restrict__ dW) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P * E) return;
+  int e = i % E;
+  double wn = sqrt(enorm[e]);
+  dW[i] += A[i] / wn - w[i] * b[e] / enorm[e];
+}
+
+constexpr int XT_TCH = 256;  // tokens per partial
+constexpr int XT_J = 64;
+constexpr int XT_C = 16;
+
+// partial[chunk][j][c] = sum_{t in chunk} X(t, j) * G(t, c)
+template <int DT>
+__global__ void __launch_bounds__(XT_J * XT_C)
+    xtg_partial_kernel(int T, int M, int NC, const void* __restrict__ X,
+                       const double* __restrict__ G, long long gst, long long gsc,
+                       double* __restrict__ part) {
+  __shared__ double xs[32][XT_J];
+  __shared__ double gs[32][XT_C];
+  const int chunk = blockIdx.z;
+  const int j0 = blockIdx.x * XT_J, c0 = blockIdx.y * XT_C;
+  const int jj = threadIdx.x % XT_J, cc = threadIdx.x / XT_J;
+  double acc = 0.0;
+  const int t_end = min(T, (chunk + 1) * XT_TCH);
+  for (int t0 = chunk * XT_TCH; t0 < t_end; t0 += 32) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * XT_J; i += XT_J * XT_C) {
+      int tt = i / XT_J, j = i % XT_J;
+      int t = t0 + tt;
+      xs[tt][j] = (t < t_end && j0 + j < M) ? load_as_double<DT>(X, static_cast<long long>(t) * M + j0 + j) : 0.0;
+    }
+    for (int i = threadIdx.x; i < 32 * XT_C; i += XT_J * XT_C) {
+      int tt = i / XT_C, c = i % XT_C;
+      int t = t0 + tt;
+      gs[tt][c] = (t < t_end && c0 + c < NC) ? G[t * gst + (c0 + c) * gsc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int tt = 0; tt < 32; ++tt) acc += xs[tt][jj] * gs[tt][cc];
+  }
+  if (j0 + jj < M && c0 + cc < NC)
+    part[(static_cast<long long>(chunk) * M + j0 + jj) * NC + c0 + cc] = acc;
+}
+
+// out[j*osj + c*osc] (+)= sum_chunk partial[chunk][j][c]  (fixed order)
+__global__ void xtg_reduce_kernel(int nchunks, int M, int NC, const double* __restrict__ part,
+                                  double* __restrict__ out, long long osj, long long osc,
+                                  int accumulate) {
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(M) * NC) return;
+  int j = static_cast<int>(i / NC), c = static_cast<int>(i % NC);
+  double a = 0.0;
+  for (int k = 0; k < nchunks; ++k) a += part[static_cast<long long>(k) * M * NC + i];
+  double* o = out + j * osj + c * osc;
+  *o = accumulate ? *o + a : a;
+}
+
+// dx[t][j] += sum_c G(t,c) * W(j,c)
+template <typename T>
+__global__ void __launch_bounds__(256)
+    dx_acc_kernel(int Tn, int M, int NC, const double* __restrict__ G, long long gst,
+                  long long gsc, const double* __restrict__ W, long long wsj, long long wsc,
+                  T* __restrict__ dx) {
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  const int t0 = blockIdx.y * 32;
+  __shared__ double gs[32][64];
+  for (int c0 = 0; c0 < NC; c0 += 64) {
+    const int nc = min(64, NC - c0);
+    double wr[64];
+    if (j < M)
+      for (int c = 0; c < nc; ++c) wr[c] = W[j * wsj + (c0 + c) * wsc];
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
+      int tt = i / 64, c = i % 64;
+      gs[tt][c] = (t0 + tt < Tn && c < nc) ? G[(t0 + tt) * gst + (c0 + c) * gsc] : 0.0;
+    }
+    __syncthreads();
+    if (j < M) {
+      for (int tt = 0; tt < 32 && t0 + tt < Tn; ++tt) {
+        double a = 0.0;
+        for (int c = 0; c < nc; ++c) a += gs[tt][c] * wr[c];
+        T* p = dx + static_cast<long long>(t0 + tt) * M + j;
+        if constexpr (sizeof(T) == 2) *p = __float2bfloat16(__bfloat162float(*p) + static_cast<float>(a));
+        else *p = static_cast<T>(static_cast<double>(*p) + a);
+      }
+    }
+  }
+}
+
+struct Ws {
+  char* p;
+  double* take(size_t n) {
+    double* r = reinterpret_cast<double*>(p);
+    p += (n * sizeof(double) + 255) & ~size_t(255);
+    return r;
+  }
+};
+
+void xtg(int xdt, int T, int M, int NC, const void* X, const double* G, long long gst,
+         long long gsc, double* out, long long osj, long long osc, int accumulate, double* part,
+         cudaStream_t st) {
+  const int nchunks = (T + XT_TCH - 1) / XT_TCH;
+  dim3 grid((M + XT_J - 1) / XT_J, (NC + XT_C - 1) / XT_C, nchunks);
+  switch (xdt) {
+    case FSMOE_F64: xtg_partial_kernel<0><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+    case FSMOE_F32: xtg_partial_kernel<1><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+    default: xtg_partial_kernel<2><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+  }
+  long long n = static_cast<long long>(M) * NC;
+  xtg_reduce_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(nchunks, M, NC, part, out,
+                                                                       osj, osc, accumulate);
+}
+
+void dx_acc(int xdt, int T, int M, int NC, const double* G, long long gst, long long gsc,
+            const double* W, long long wsj, long long wsc, void* dx, cudaStream_t st) {
+  dim3 grid((M + 255) / 256, (T + 31) / 32);
+  switch (xdt) {
+    case FSMOE_F64: dx_acc_kernel<double><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<double*>(dx)); break;
+    case FSMOE_F32: dx_acc_kernel<float><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<float*>(dx)); break;
+    default: dx_acc_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<__nv_bfloat16*>(dx)); break;
+  }
+}
+
+}  // namespace
+
+size_t gate_bwd_workspace_bytes(const fsmoe_gate_desc& d) {
+  const size_t T = d.tokens, E = d.score_cols, M = d.model_dim, P = d.proj_rows > 0 ? d.proj_rows : 0;
+  const size_t nch = (T + XT_TCH - 1) / XT_TCH;
+  size_t nc = E > P ? E : P;
+  size_t wide = M > P ? M : P;
+  auto r = [](size_t n) { return (n * 8 + 255) & ~size_t(255); };
+  return r(T * E) * 2 + r(T * P) * 2 + r(nch * wide * (nc > 0 ? nc : 1)) + r(P * E) + r(E) * 2 + 1024;
+}
+
+int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
+                    const double* w_noise, const double* proj, const int* ptok, const int* pexp,
+                    const double* pw, const double* dw, const double* scores, const double* noise,
+                    const double* spread, const double* proj_out, void* dx, double* dWs,
+                    double* dWn, double* dP, void* ws, cudaStream_t st) {
+  const int T = d.tokens, M = d.model_dim, E = d.score_cols, k = d.top_k;
+  Ws w{static_cast<char*>(ws)};
+  double* dS = w.take(static_cast<size_t>(T) * E);
+  const int nch = (T + XT_TCH - 1) / XT_TCH;
+  const int P = d.proj_rows > 0 ? d.proj_rows : 0;
+  const int nc = E > P ? E : P;
+  double* part = w.take(static_cast<size_t>(nch) * (M > P ? M : P) * (nc > 0 ? nc : 1));
+  switch (d.kind) {
+    case FSMOE_GATE_NOISY_TOPK: {
+      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS);
+      double* dZ = w.take(static_cast<size_t>(T) * E);
+      long long n = static_cast<long long>(T) * E;
+      noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ);
+      xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
+      xtg(d.x_dtype, T, M, E, x, dZ, E, 1, dWn, E, 1, 1, part, st);
+      dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
+      dx_acc(d.x_dtype, T, M, E, dZ, E, 1, w_noise, E, 1, dx, st);
+      break;
+    }
+    case FSMOE_GATE_SIGMOID_TOPK: {
+      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(1, T, E, k, pexp, pw, dw, dS);
+      xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
+      dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
+      break;
+    }
+    case FSMOE_GATE_EXPERT_CHOICE: {
+      dscore_ec_kernel<<<E, 256, 0, st>>>(T, E, k, ptok, pw, dw, dS);  // E x T
+      xtg(d.x_dtype, T, M, E, x, dS, 1, T, dWs, E, 1, 1, part, st);
+      dx_acc(d.x_dtype, T, M, E, dS, 1, T, w_score, E, 1, dx, st);
+      break;
+    }
+    case FSMOE_GATE_COSINE_TOPK: {
+      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS);
+      double* dq = w.take(static_cast<size_t>(T) * P);
+      double* qn = w.take(static_cast<size_t>(T) * P);
+      double* en = w.take(E);
+      double* bb = w.take(E);
+      double* A = w.take(static_cast<size_t>(P) * E);
+      // enorm recomputed (cheap) with the forward's arithmetic
+      cosine_enorm(P, E, w_score, en, st);
+      cosine_dq_kernel<<<(T + 127) / 128, 128, 0, st>>>(T, E, P, proj_out, w_score, en, scores, dS,
+                                                       dq, qn);
+      cosine_b_kernel<<<E, 256, 0, st>>>(T, E, scores, dS, bb);
+      xtg(FSMOE_F64, T, P, E, qn, dS, E, 1, A, E, 1, 0, part, st);
+      cosine_dw_kernel<<<(P * E + 255) / 256, 256, 0, st>>>(P, E, A, w_score, en, bb, dWs);
+      // dProj[p][j] += sum_t dq[t][p] x[t][j]
+      xtg(d.x_dtype, T, M, P, x, dq, P, 1, dP, 1, M, 1, part, st);
+      // dx += dq . Proj  (W(j,p) = Proj[p*M + j])
+      dx_acc(d.x_dtype, T, M, P, dq, P, 1, proj, 1, M, dx, st);
+      break;
+    }
+    default:
+      return config_error("gate: unknown gate kind");
+  }
+  return cuda_status(cudaGetLastError(), "fsmoe_gate_bwd");
+}
+
+}  // namespace fsmoe

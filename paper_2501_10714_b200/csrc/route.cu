@@ -1,0 +1,486 @@
+// route.cu — K2 capacity assignment, K3 dispatch (Order), K5 combine
+// (I-Order) and their backward, for /root/reference/proj/src/workload.cpp:
+//   dispatch_tokens 237-264  ->  assign_{count,rank}_kernel + dispatch_kernel
+//   combine_tokens  266-282  ->  combine_kernel
+//
+// Assignment is a stable per-expert rank over the pick sequence (the
+// reference's sequential fill loop): ranks inside 32-pick warp windows come
+// from __match_any_sync, across warps/rounds from shared-memory prefix sums,
+// across tiles from per-tile expert histograms. No atomics decide order, so
+// slot_of_pick / fill / dropped are bit-identical to the reference.
+//
+// Permutation kernels move one buffer row per warp with 16-byte vector
+// accesses (rows are contiguous, so each warp-instruction covers 512 B).
+// Combine / dispatch-backward gather the (<= k) rows of a token and reduce in
+// pick order; fp64 uses separately rounded multiply and add exactly as the
+// reference (y[t] += w * buf[slot]).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "capi_common.h"
+#include "kernels.h"
+#include "route_common.cuh"
+
+namespace fsmoe {
+namespace {
+
+using namespace fsmoe_dev;
+
+constexpr int AS_THREADS = 1024;
+constexpr int AS_TILE = 4 * AS_THREADS;  // picks per tile
+constexpr int AS_MAX_E = 256;
+
+// cnt[tile][e] = picks of expert e inside the tile; flags bad picks.
+__global__ void __launch_bounds__(AS_THREADS)
+    assign_count_kernel(long long P, const int* __restrict__ ptok, const int* __restrict__ pexp,
+                        int T, int E, int* __restrict__ cnt, int* __restrict__ status) {
+  __shared__ int h[AS_MAX_E];
+  for (int i = threadIdx.x; i < E; i += AS_THREADS) h[i] = 0;
+  __syncthreads();
+  const long long base = static_cast<long long>(blockIdx.x) * AS_TILE;
+  for (int i = threadIdx.x; i < AS_TILE; i += AS_THREADS) {
+    long long p = base + i;
+    if (p >= P) break;
+    int e = pexp[p], t = ptok[p];
+    if (e < 0 || e >= E || t < 0 || t >= T) {
+      if (status) atomicOr(status, 8);
+      continue;
+    }
+    atomicAdd(&h[e], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += AS_THREADS) cnt[blockIdx.x * E + i] = h[i];
+}
+
+__global__ void __launch_bounds__(AS_THREADS)
+    assign_rank_kernel(long long P, const int* __restrict__ pexp, int E, long long C,
+                       const int* __restrict__ cnt, int ntiles, int* __restrict__ slot_of_pick,
+                       int* __restrict__ pick_of_slot, long long* __restrict__ fill,
+                       long long* __restrict__ dropped) {
+  __shared__ int base[AS_MAX_E];
+  __shared__ int wc[AS_THREADS / 32][AS_MAX_E];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < E; e += AS_THREADS) {
+    int b = 0;
+    for (int tl = 0; tl < static_cast<int>(blockIdx.x); ++tl) b += cnt[tl * E + e];
+    base[e] = b;
+    if (blockIdx.x == 0) {
+      long long tot = 0;
+      for (int tl = 0; tl < ntiles; ++tl) tot += cnt[tl * E + e];
+      fill[e] = tot < C ? tot : C;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long d = 0;
+    for (int e = 0; e < E; ++e) {
+      long long tot = 0;
+      for (int tl = 0; tl < ntiles; ++tl) tot += cnt[tl * E + e];
+      d += tot > C ? tot - C : 0;
+    }
+    *dropped = d;
+  }
+  const long long tile0 = static_cast<long long>(blockIdx.x) * AS_TILE;
+  for (int r = 0; r < AS_TILE / AS_THREADS; ++r) {
+    for (int i = threadIdx.x; i < (AS_THREADS / 32) * E; i += AS_THREADS) wc[i / E][i % E] = 0;
+    __syncthreads();
+    long long p = tile0 + static_cast<long long>(r) * AS_THREADS + threadIdx.x;
+    int e = -1;
+    if (p < P) {
+      e = pexp[p];
+      if (e < 0 || e >= E) e = -1;
+    }
+    unsigned same = __match_any_sync(0xffffffffu, e);
+    int in_warp = __popc(same & ((1u << lane) - 1u));
+    if (e >= 0 && in_warp == 0) wc[wid][e] = __popc(same);
+    __syncthreads();
+    if (e >= 0) {
+      int rank = base[e] + in_warp;
+      for (int w = 0; w < wid; ++w) rank += wc[w][e];
+      if (rank < C) {
+        long long slot = static_cast<long long>(e) * C + rank;
+        slot_of_pick[p] = static_cast<int>(slot);
+        pick_of_slot[slot] = static_cast<int>(p);
+      } else {
+        slot_of_pick[p] = -1;
+      }
+    } else if (p < P) {
+      slot_of_pick[p] = -1;
+    }
+    __syncthreads();
+    for (int ee = threadIdx.x; ee < E; ee += AS_THREADS) {
+      int s = 0;
+      for (int w = 0; w < AS_THREADS / 32; ++w) s += wc[w][ee];
+      base[ee] += s;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------ token index (CSR) --
+
+__global__ void tok_token_major_kernel(int T, int k, int* __restrict__ ptr, int* __restrict__ idx) {
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i <= T) ptr[i] = static_cast<int>(i * k);
+  if (i < static_cast<long long>(T) * k) idx[i] = static_cast<int>(i);
+}
+
+__global__ void tok_count_kernel(long long P, const int* __restrict__ ptok, int T,
+                                 int* __restrict__ cnt) {
+  long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (p < P) {
+    int t = ptok[p];
+    if (t >= 0 && t < T) atomicAdd(&cnt[t], 1);
+  }
+}
+
+// Single-block exclusive scan of n ints (n up to a few 1e5; used once per layer).
+__global__ void __launch_bounds__(1024) scan_excl_kernel(const int* __restrict__ in, int n,
+                                                         int* __restrict__ out) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int b = 0; b < n; b += 1024) {
+    int i = b + threadIdx.x;
+    int v = i < n ? in[i] : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = warp_tot[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;
+    }
+    __syncthreads();
+    int before = (wid > 0 ? warp_tot[wid - 1] : 0) + carry;
+    if (i < n) out[i] = before + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_tot[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+__global__ void tok_place_kernel(long long P, const int* __restrict__ ptok, int T,
+                                 const int* __restrict__ ptr, int* __restrict__ cursor,
+                                 int* __restrict__ idx) {
+  long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (p < P) {
+    int t = ptok[p];
+    if (t >= 0 && t < T) idx[ptr[t] + atomicAdd(&cursor[t], 1)] = static_cast<int>(p);
+  }
+}
+
+// Per-token insertion sort: lists are short (<= experts), restores pick order.
+__global__ void tok_sort_kernel(int T, const int* __restrict__ ptr, int* __restrict__ idx) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int a = ptr[t], b = ptr[t + 1];
+  for (int i = a + 1; i < b; ++i) {
+    int v = idx[i], j = i - 1;
+    while (j >= a && idx[j] > v) {
+      idx[j + 1] = idx[j];
+      --j;
+    }
+    idx[j + 1] = v;
+  }
+}
+
+// --------------------------------------------------------------- dispatch --
+
+// buffers[row(s)] = x[token(pick_of_slot[s])] or 0; one warp per slot row.
+template <typename V>
+__global__ void __launch_bounds__(256)
+    dispatch_kernel(long long n_slots, int row_vecs, int E, long long C, int chunks,
+                    const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
+                    const V* __restrict__ x, V* __restrict__ buf) {
+  const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (s >= n_slots) return;
+  const int lane = threadIdx.x & 31;
+  const int p = pick_of_slot[s];
+  V* dst = buf + slot_row(s, E, C, chunks) * row_vecs;
+  if (p < 0) {
+    V z;
+    memset(&z, 0, sizeof(V));
+    for (int i = lane; i < row_vecs; i += 32) dst[i] = z;
+    return;
+  }
+  const V* src = x + static_cast<long long>(ptok[p]) * row_vecs;
+  for (int i = lane; i < row_vecs; i += 32) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------- combine --
+
+template <typename T>
+struct Acc;
+template <>
+struct Acc<double> {
+  using type = double;
+  static __device__ __forceinline__ double ld(const double* p, int i) { return p[i]; }
+  static __device__ __forceinline__ void st(double* p, int i, double v) { p[i] = v; }
+};
+template <>
+struct Acc<float> {
+  using type = float;
+  static __device__ __forceinline__ float ld(const float* p, int i) { return p[i]; }
+  static __device__ __forceinline__ void st(float* p, int i, float v) { p[i] = v; }
+};
+template <>
+struct Acc<__nv_bfloat16> {
+  using type = float;
+  static __device__ __forceinline__ float ld(const __nv_bfloat16* p, int i) {
+    return __bfloat162float(p[i]);
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, int i, float v) {
+    p[i] = __float2bfloat16(v);
+  }
+};
+
+__device__ __forceinline__ double madd(double acc, double w, double b) {
+  return __dadd_rn(acc, __dmul_rn(w, b));
+}
+__device__ __forceinline__ float madd(float acc, float w, float b) { return fmaf(w, b, acc); }
+
+// 8 elements per lane per step (16 B of bf16 / 32 B fp32 / 64 B fp64).
+constexpr int CV = 8;
+
+// y[t] = sum_{kept picks of t, pick order} w * buf[row(slot)]; one warp per token.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    combine_kernel(int ntok, int M, int E, long long C, int chunks, const int* __restrict__ tptr,
+                   const int* __restrict__ tpick, const int* __restrict__ slot_of_pick,
+                   const double* __restrict__ pw, const T* __restrict__ buf, T* __restrict__ y) {
+  using A = typename Acc<T>::type;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= ntok) return;
+  const int lane = threadIdx.x & 31;
+  const int a = tptr[t], b = tptr[t + 1];
+  T* yr = y + static_cast<long long>(t) * M;
+  for (int j0 = lane * CV; j0 < M; j0 += 32 * CV) {
+    A acc[CV];
+#pragma unroll
+    for (int v = 0; v < CV; ++v) acc[v] = A(0);
+    for (int q = a; q < b; ++q) {
+      const int p = tpick[q];
+      const int s = slot_of_pick[p];
+      if (s < 0) continue;
+      const A w = static_cast<A>(pw[p]);
+      const T* br = buf + slot_row(s, E, C, chunks) * M;
+#pragma unroll
+      for (int v = 0; v < CV; ++v)
+        if (j0 + v < M) acc[v] = madd(acc[v], w, Acc<T>::ld(br, j0 + v));
+    }
+#pragma unroll
+    for (int v = 0; v < CV; ++v)
+      if (j0 + v < M) Acc<T>::st(yr, j0 + v, acc[v]);
+  }
+}
+
+// dx[t] (+)= sum_{kept picks of t} dbuf[row(slot)]
+template <typename T>
+__global__ void __launch_bounds__(256)
+    dispatch_bwd_kernel(int ntok, int M, int E, long long C, int chunks,
+                        const int* __restrict__ tptr, const int* __restrict__ tpick,
+                        const int* __restrict__ slot_of_pick, const T* __restrict__ dbuf,
+                        T* __restrict__ dx, int accumulate) {
+  using A = typename Acc<T>::type;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= ntok) return;
+  const int lane = threadIdx.x & 31;
+  const int a = tptr[t], b = tptr[t + 1];
+  T* xr = dx + static_cast<long long>(t) * M;
+  for (int j0 = lane * CV; j0 < M; j0 += 32 * CV) {
+    A acc[CV];
+#pragma unroll
+    for (int v = 0; v < CV; ++v) acc[v] = (accumulate && j0 + v < M) ? Acc<T>::ld(xr, j0 + v) : A(0);
+    for (int q = a; q < b; ++q) {
+      const int s = slot_of_pick[tpick[q]];
+      if (s < 0) continue;
+      const T* br = dbuf + slot_row(s, E, C, chunks) * M;
+#pragma unroll
+      for (int v = 0; v < CV; ++v)
+        if (j0 + v < M) acc[v] = acc[v] + Acc<T>::ld(br, j0 + v);
+    }
+#pragma unroll
+    for (int v = 0; v < CV; ++v)
+      if (j0 + v < M) Acc<T>::st(xr, j0 + v, acc[v]);
+  }
+}
+
+// dbuf[row(s)] = w_p * dy[t_p] (0 for padding); dw[p] = <dy[t_p], buf[row(s)]>.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    combine_bwd_kernel(long long n_slots, int M, int E, long long C, int chunks,
+                       const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
+                       const double* __restrict__ pw, const T* __restrict__ dy,
+                       const T* __restrict__ buf, T* __restrict__ dbuf, double* __restrict__ dw) {
+  using A = typename Acc<T>::type;
+  const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (s >= n_slots) return;
+  const int lane = threadIdx.x & 31;
+  const int p = pick_of_slot[s];
+  const long long row = slot_row(s, E, C, chunks);
+  T* dr = dbuf + row * M;
+  if (p < 0) {
+    for (int j = lane; j < M; j += 32) Acc<T>::st(dr, j, A(0));
+    return;
+  }
+  const A w = static_cast<A>(pw[p]);
+  const T* g = dy + static_cast<long long>(ptok[p]) * M;
+  const T* o = buf + row * M;
+  A dot = A(0);
+  for (int j0 = lane * CV; j0 < M; j0 += 32 * CV) {
+#pragma unroll
+    for (int v = 0; v < CV; ++v) {
+      if (j0 + v >= M) break;
+      A gv = Acc<T>::ld(g, j0 + v);
+      Acc<T>::st(dr, j0 + v, static_cast<A>(w * gv));
+      dot = madd(dot, gv, Acc<T>::ld(o, j0 + v));
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+  if (lane == 0) dw[p] = static_cast<double>(dot);
+}
+
+template <typename F>
+int by_dtype(int dtype, F&& f) {
+  switch (dtype) {
+    case FSMOE_F64: f(double{}); return 0;
+    case FSMOE_F32: f(float{}); return 0;
+    case FSMOE_BF16: f(__nv_bfloat16{}); return 0;
+    default: return -1;
+  }
+}
+
+int elem_size(int dtype) { return dtype == FSMOE_F64 ? 8 : dtype == FSMOE_F32 ? 4 : 2; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ host ---
+
+size_t assign_workspace_bytes(long long P, int E) {
+  long long ntiles = (P + AS_TILE - 1) / AS_TILE;
+  if (ntiles < 1) ntiles = 1;
+  return static_cast<size_t>(ntiles) * (E > 0 ? E : 1) * sizeof(int) + 256;
+}
+
+int assign_launch(long long P, const int* ptok, const int* pexp, int T, int E, long long C,
+                  int* slot_of_pick, long long* fill, long long* dropped, int* pick_of_slot,
+                  int* status, void* ws, cudaStream_t st) {
+  if (E > AS_MAX_E) return config_error("dispatch: at most 256 experts per rank supported");
+  FSMOE_CUDA_TRY(cudaMemsetAsync(pick_of_slot, 0xFF, sizeof(int) * E * C, st), "assign memset");
+  if (P <= 0) {
+    FSMOE_CUDA_TRY(cudaMemsetAsync(fill, 0, sizeof(long long) * E, st), "assign memset");
+    FSMOE_CUDA_TRY(cudaMemsetAsync(dropped, 0, sizeof(long long), st), "assign memset");
+    return FSMOE_OK;
+  }
+  int ntiles = static_cast<int>((P + AS_TILE - 1) / AS_TILE);
+  int* cnt = static_cast<int*>(ws);
+  assign_count_kernel<<<ntiles, AS_THREADS, 0, st>>>(P, ptok, pexp, T, E, cnt, status);
+  assign_rank_kernel<<<ntiles, AS_THREADS, 0, st>>>(P, pexp, E, C, cnt, ntiles, slot_of_pick,
+                                                    pick_of_slot, fill, dropped);
+  return cuda_status(cudaGetLastError(), "fsmoe_assign");
+}
+
+size_t token_index_workspace_bytes(long long, int T) {
+  return static_cast<size_t>(T + 1) * sizeof(int) * 2 + 256;
+}
+
+int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, int* tpick,
+                       void* ws, cudaStream_t st) {
+  if (k > 0) {
+    long long n = (static_cast<long long>(T) * k > T + 1) ? static_cast<long long>(T) * k : T + 1;
+    tok_token_major_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(T, k, tptr, tpick);
+    return cuda_status(cudaGetLastError(), "fsmoe_token_index");
+  }
+  int* cnt = static_cast<int*>(ws);
+  int* cursor = cnt + (T + 1);
+  FSMOE_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (T + 1) * 2, st), "token_index memset");
+  int pb = static_cast<int>((P + 255) / 256);
+  if (pb > 0) tok_count_kernel<<<pb, 256, 0, st>>>(P, ptok, T, cnt);
+  scan_excl_kernel<<<1, 1024, 0, st>>>(cnt, T, tptr);
+  if (pb > 0) tok_place_kernel<<<pb, 256, 0, st>>>(P, ptok, T, tptr, cursor, tpick);
+  tok_sort_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, tptr, tpick);
+  return cuda_status(cudaGetLastError(), "fsmoe_token_index");
+}
+
+int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int* pick_of_slot,
+                    const int* ptok, const void* x, void* buf, cudaStream_t st) {
+  const long long n_slots = static_cast<long long>(E) * C;
+  if (n_slots <= 0 || M <= 0) return FSMOE_OK;
+  const long long row_bytes = static_cast<long long>(M) * elem_size(dtype);
+  const int grid = static_cast<int>((n_slots + 7) / 8);
+  if (row_bytes % 16 == 0) {
+    dispatch_kernel<uint4><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 16), E, C,
+                                                 chunks, pick_of_slot, ptok,
+                                                 static_cast<const uint4*>(x), static_cast<uint4*>(buf));
+  } else if (row_bytes % 8 == 0) {
+    dispatch_kernel<uint2><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 8), E, C,
+                                                 chunks, pick_of_slot, ptok,
+                                                 static_cast<const uint2*>(x), static_cast<uint2*>(buf));
+  } else {
+    dispatch_kernel<uint16_t><<<grid, 256, 0, st>>>(
+        n_slots, static_cast<int>(row_bytes / 2), E, C, chunks, pick_of_slot, ptok,
+        static_cast<const uint16_t*>(x), static_cast<uint16_t*>(buf));
+  }
+  return cuda_status(cudaGetLastError(), "fsmoe_dispatch");
+}
+
+int combine_launch(int dtype, int T, int M, int E, long long C, int chunks, const int* tptr,
+                   const int* tpick, const int* slot_of_pick, const double* pw, const void* buf,
+                   void* y, cudaStream_t st) {
+  if (T <= 0 || M <= 0) return FSMOE_OK;
+  const int grid = (T + 7) / 8;
+  int rc = by_dtype(dtype, [&](auto tag) {
+    using Tt = decltype(tag);
+    combine_kernel<Tt><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick, pw,
+                                             static_cast<const Tt*>(buf), static_cast<Tt*>(y));
+  });
+  if (rc) return config_error("combine: unknown dtype");
+  return cuda_status(cudaGetLastError(), "fsmoe_combine");
+}
+
+int dispatch_bwd_launch(int dtype, int T, int M, int E, long long C, int chunks, const int* tptr,
+                        const int* tpick, const int* slot_of_pick, const void* dbuf, void* dx,
+                        int accumulate, cudaStream_t st) {
+  if (T <= 0 || M <= 0) return FSMOE_OK;
+  const int grid = (T + 7) / 8;
+  int rc = by_dtype(dtype, [&](auto tag) {
+    using Tt = decltype(tag);
+    dispatch_bwd_kernel<Tt><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+                                                  static_cast<const Tt*>(dbuf),
+                                                  static_cast<Tt*>(dx), accumulate);
+  });
+  if (rc) return config_error("dispatch_bwd: unknown dtype");
+  return cuda_status(cudaGetLastError(), "fsmoe_dispatch_bwd");
+}
+
+int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long long P,
+                       const int* pick_of_slot, const int* ptok, const double* pw,
+                       const void* dy, const void* buf, void* dbuf, double* dw, cudaStream_t st) {
+  const long long n_slots = static_cast<long long>(E) * C;
+  if (P > 0) FSMOE_CUDA_TRY(cudaMemsetAsync(dw, 0, sizeof(double) * P, st), "combine_bwd memset");
+  if (n_slots <= 0 || M <= 0) return FSMOE_OK;
+  const int grid = static_cast<int>((n_slots + 7) / 8);
+  int rc = by_dtype(dtype, [&](auto tag) {
+    using Tt = decltype(tag);
+    combine_bwd_kernel<Tt><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
+                                                 static_cast<const Tt*>(dy),
+                                                 static_cast<const Tt*>(buf),
+                                                 static_cast<Tt*>(dbuf), dw);
+  });
+  if (rc) return config_error("combine_bwd: unknown dtype");
+  return cuda_status(cudaGetLastError(), "fsmoe_combine_bwd");
+}
+
+}  // namespace fsmoe
