@@ -44,6 +44,10 @@ enum fsmoe_dtype { FSMOE_F64 = 0, FSMOE_F32 = 1, FSMOE_BF16 = 2 };
 
 const char* fsmoe_last_error(void);
 int fsmoe_abi_version(void);
+/* Utilities: stream-ordered device-to-device copy; select the CUDA device of
+ * the calling thread. */
+int fsmoe_copy_device(void* dst, const void* src, size_t bytes, void* stream);
+int fsmoe_set_device(int device);
 
 /* ---------------------------------------------------------------- routing --
  * Replaces fsmoe::run_gate (workload.hpp:110-111, workload.cpp:143-235).
@@ -163,6 +167,8 @@ int fsmoe_gate_bwd(const fsmoe_gate_desc* d, const void* x, const double* w_scor
 typedef struct fsmoe_gemm_desc {
   int kind;        /* 0 row-grouped (fwd/dgrad), 1 k-grouped (wgrad) */
   int nblk, rows, K, N, Mo, No, n_w;
+  int rows_total;  /* rows per block in memory (0 -> rows) */
+  int row0;        /* first processed row of each block (pipeline chunk) */
   int b_mn_major;
   const void* A;
   const void* B;
@@ -180,9 +186,10 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream);
 
 /* Elementwise activation kernels used by the fp32 check mode
  * (op: 2 gelu fwd, 3 swiglu fwd, 4 gelu bwd, 5 swiglu bwd; same layouts as
- * the fused tcgen05 epilogues). */
-int fsmoe_activation_f32(int op, long long rows, int units, const float* in, const float* z,
-                         float* out, float* out2, void* stream);
+ * the fused tcgen05 epilogues), over rows [row0, row0+rows) of nblk blocks of
+ * rows_total rows. */
+int fsmoe_activation_f32(int op, int nblk, int rows_total, int row0, int rows, int units,
+                         const float* in, const float* z, float* out, void* stream);
 
 #ifdef __cplusplus
 }

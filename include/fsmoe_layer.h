@@ -1,0 +1,77 @@
+/*
+ * fsmoe_layer.h — C ABI of libfsmoe.so: the unified MoE layer (C++
+ * fsmoe::MoELayer, include/fsmoe/moe_layer.hpp) and the expert-parallel NCCL
+ * group, for hosts that bind through an FFI (ctypes here; see INTEGRATION.md
+ * for the cgo / JNI shape of the same calls).
+ *
+ * Status codes as include/fsmoe_cuda.h (0 ok, 2 config, 3 fit quality,
+ * 4 invariant, 5 device); message via fsmoe_layer_last_error().
+ */
+#ifndef FSMOE_LAYER_H
+#define FSMOE_LAYER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fsmoe_ep fsmoe_ep;
+typedef struct fsmoe_layer fsmoe_layer;
+
+typedef struct fsmoe_layer_config {
+  int tokens;          /* local tokens per rank */
+  int model_dim;       /* M */
+  int ffn_dim;         /* H */
+  int experts;         /* E, global */
+  int top_k;
+  int gate_kind;       /* enum fsmoe_gate_kind */
+  int ffn_kind;        /* 0 simple (2 GEMMs, GELU), 1 gated3 (3 GEMMs, SwiGLU) */
+  long long capacity;  /* per (rank, expert); 0 -> capacity_tokens(k, f = 1) */
+  int proj_dim;        /* cosine_topk projection rows */
+  uint64_t seed;       /* noisy_topk noise seed */
+  int precision;       /* 0 bf16 (tcgen05), 1 fp32 check mode */
+  int r_fwd, r_bwd;    /* pipeline degrees */
+  int device;
+  long long dense_grad_elems;   /* optional replicated fp32 gradient, allreduced in slices */
+  int n_ar_slices;
+  const long long* ar_slices;   /* slice sizes (elements), n_ar_slices entries */
+} fsmoe_layer_config;
+
+typedef struct fsmoe_layer_params {
+  double* w_gate;   /* score weights M x E (cosine: proj_dim x E), fp64 */
+  double* w_noise;  /* M x E fp64 (noisy_topk) */
+  double* proj;     /* proj_dim x M fp64 (cosine_topk) */
+  void* w1;         /* [E_local][N1][M], N1 = H or 2H (gated3, 128-unit gate/up interleave) */
+  void* w2;         /* [E_local][M][H] */
+  double* g_gate;
+  double* g_noise;
+  double* g_proj;
+  float* g_w1;
+  float* g_w2;
+  float* dense_grad;
+} fsmoe_layer_params;
+
+const char* fsmoe_layer_last_error(void);
+
+/* NCCL bootstrap: rank 0 creates the id, the host broadcasts it. */
+int fsmoe_ep_unique_id(unsigned char out[128]);
+int fsmoe_ep_create(int world, int rank, const unsigned char id[128], int device, int max_ctas,
+                    fsmoe_ep** out);
+int fsmoe_ep_destroy(fsmoe_ep* ep);
+
+/* ep may be NULL (single GPU, all experts local). */
+int fsmoe_layer_create(const fsmoe_layer_config* cfg, fsmoe_ep* ep, fsmoe_layer** out);
+int fsmoe_layer_destroy(fsmoe_layer* layer);
+int fsmoe_layer_bind(fsmoe_layer* layer, const fsmoe_layer_params* params);
+long long fsmoe_layer_capacity(const fsmoe_layer* layer);
+int fsmoe_layer_forward(fsmoe_layer* layer, const void* x, void* y, void* stream);
+int fsmoe_layer_backward(fsmoe_layer* layer, const void* dy, void* dx, void* stream);
+/* Named internal device buffer (pick_token, slot_of_pick, fill, X_send, Z, ...). */
+int fsmoe_layer_buffer(const fsmoe_layer* layer, const char* name, void** ptr, long long* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

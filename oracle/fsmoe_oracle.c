@@ -63,6 +63,14 @@ double orc_normal_next(orc_mt64* g) {
   return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793238462643383279502884 * u2);
 }
 
+/* The noise row of token t (workload.cpp:184-186): E draws of
+ * NormalDraws(seed + t), in expert order. */
+void orc_noise_row(uint64_t seed, int t, int E, double* out) {
+  orc_mt64 g;
+  orc_mt64_seed(&g, seed + (uint64_t)t);
+  for (int e = 0; e < E; ++e) out[e] = orc_normal_next(&g);
+}
+
 /* -------------------------------------------------------------- helpers -- */
 
 static int fail(char* err, int errlen, const char* msg) {

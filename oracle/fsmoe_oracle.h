@@ -42,6 +42,9 @@ void orc_uniform_fill(orc_mt64* g, long long n, double lo, double hi, double* ou
 /* Box-Muller normal draw, workload.cpp:90-95. */
 double orc_normal_next(orc_mt64* g);
 
+/* E normal draws of NormalDraws(seed + t) (workload.cpp:184-186). */
+void orc_noise_row(uint64_t seed, int t, int E, double* out);
+
 /* capacity_tokens, workload.cpp:43-51. Returns -1 and fills err on ConfigError. */
 long long orc_capacity_tokens(int batch, int heads, int seq_len, int model_dim,
                               int hidden_scale, double capacity_factor,

@@ -39,7 +39,7 @@ class GemmDesc(C.Structure):
     _fields_ = [
         ("kind", C.c_int), ("nblk", C.c_int), ("rows", C.c_int), ("K", C.c_int),
         ("N", C.c_int), ("Mo", C.c_int), ("No", C.c_int), ("n_w", C.c_int),
-        ("b_mn_major", C.c_int), ("A", C.c_void_p), ("B", C.c_void_p),
+        ("rows_total", C.c_int), ("row0", C.c_int), ("b_mn_major", C.c_int), ("A", C.c_void_p), ("B", C.c_void_p),
         ("valid_rows", C.c_void_p), ("epi", C.c_int), ("D", C.c_void_p), ("D2", C.c_void_p),
         ("Zin", C.c_void_p), ("ldd", C.c_longlong), ("ldd2", C.c_longlong),
         ("ldz", C.c_longlong), ("accumulate", C.c_int), ("precision", C.c_int),

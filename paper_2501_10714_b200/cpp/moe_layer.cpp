@@ -1,0 +1,550 @@
+// moe_layer.cpp — the MoE layer executor (include/fsmoe/moe_layer.hpp).
+//
+// Per rank, canonical buffer layout [src rank p][local expert e_l][capacity C]
+// rows of width M (send side: [expert e][C], e = p*E_l + e_l, which is the same
+// thing). A pipeline chunk i is the row window [lo_i, hi_i) of every block,
+// lo/hi on 128-row granules, so a chunk's AlltoAll is E grouped
+// ncclSend/ncclRecv pairs of (hi-lo)*M elements and its expert GEMMs are one
+// grouped-GEMM launch over the window (GemmProblem::row0/rows). Forward and
+// backward degrees are independent (r_fwd != r_bwd), as in FSMoE.
+//
+// Streams: compute (gate, permutations, GEMMs) and comm (NCCL), joined by
+// events; the comm stream's FIFO order is the schedule simulator's inter-link
+// emission order: dispatch 0..r-1, [gradient allreduce slices], combine
+// 0..r-1 (schedule_sim.cpp:182-216).
+#include "fsmoe/moe_layer.hpp"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+
+#include "device_util.hpp"
+#include "ep_group.hpp"
+#include "fsmoe_cuda.h"
+
+namespace fsmoe {
+
+namespace {
+
+int gate_kind_abi(GateKind k) {
+  switch (k) {
+    case GateKind::noisy_topk: return FSMOE_GATE_NOISY_TOPK;
+    case GateKind::sigmoid_topk: return FSMOE_GATE_SIGMOID_TOPK;
+    case GateKind::cosine_topk: return FSMOE_GATE_COSINE_TOPK;
+    case GateKind::expert_choice: return FSMOE_GATE_EXPERT_CHOICE;
+  }
+  return -1;
+}
+
+struct Chunk {
+  int lo, hi;
+};
+
+// 128-row granule chunks of [0, C): r clipped to the granule count.
+std::vector<Chunk> make_chunks(long long C, int r) {
+  const long long ng = (C + 127) / 128;
+  if (r < 1) r = 1;
+  if (r > ng) r = static_cast<int>(ng);
+  std::vector<Chunk> out;
+  for (int i = 0; i < r; ++i) {
+    long long a = (i * ng) / r * 128, b = ((i + 1) * ng) / r * 128;
+    out.push_back({static_cast<int>(a), static_cast<int>(std::min(b, C))});
+  }
+  return out;
+}
+
+}  // namespace
+
+struct MoELayer::Impl {
+  MoELayerConfig cfg;
+  EpGroup* ep = nullptr;
+  int P = 1, rank = 0, E = 0, El = 0, T = 0, M = 0, H = 0, N1 = 0, k = 0;
+  long long C = 0, n_picks = 0;
+  int esz = 2;          // activation element size
+  int dtype = FSMOE_BF16;
+  ncclDataType_t nccl_dt = ncclBfloat16;
+  fsmoe_gate_desc gd{};
+  MoEParams prm;
+  const void* x_last = nullptr;  // forward input (caller keeps it alive for backward)
+  std::vector<Chunk> fwd_chunks, bwd_chunks;
+
+  cudaStream_t s_comp = nullptr, s_comm = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_gate = nullptr, ev_join = nullptr;
+  std::vector<cudaEvent_t> ev_a, ev_b;  // per-chunk (max of r_fwd, r_bwd)
+
+  std::map<std::string, std::pair<void*, long long>> bufs;
+  std::vector<void*> owned;
+
+  // routing state
+  int *tok = nullptr, *exp = nullptr, *slot = nullptr, *pos = nullptr, *tptr = nullptr,
+      *tpick = nullptr, *status = nullptr;
+  double *w = nullptr, *dw = nullptr, *scores = nullptr, *noise = nullptr, *spread = nullptr,
+         *proj_out = nullptr;
+  long long *fill = nullptr, *dropped = nullptr, *rfill = nullptr;
+  void *gate_ws = nullptr, *assign_ws = nullptr, *tidx_ws = nullptr, *gbwd_ws = nullptr;
+  size_t gate_wsb = 0, assign_wsb = 0, tidx_wsb = 0, gbwd_wsb = 0;
+  // activations (canonical [P*E_l][C][.])
+  void *Xs = nullptr, *Xr = nullptr, *Z = nullptr, *Hh = nullptr, *Or = nullptr, *Os = nullptr;
+  void *dOs = nullptr, *dOr = nullptr, *dXr = nullptr, *dXs = nullptr;
+
+  void* dalloc(const std::string& name, long long bytes) {
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, static_cast<size_t>(std::max<long long>(bytes, 16))), "cudaMalloc");
+    owned.push_back(p);
+    bufs[name] = {p, bytes};
+    return p;
+  }
+  void alias(const std::string& name, void* p, long long bytes) { bufs[name] = {p, bytes}; }
+
+  ~Impl() {
+    if (s_comp) cudaStreamSynchronize(s_comp);
+    if (s_comm) cudaStreamSynchronize(s_comm);
+    for (void* p : owned) cudaFree(p);
+    for (auto e : ev_a) cudaEventDestroy(e);
+    for (auto e : ev_b) cudaEventDestroy(e);
+    for (auto e : {ev_in, ev_out, ev_gate, ev_join})
+      if (e) cudaEventDestroy(e);
+    if (s_comp) cudaStreamDestroy(s_comp);
+    if (s_comm) cudaStreamDestroy(s_comm);
+  }
+
+  // ------------------------------------------------------------- GEMMs --
+  void gemm(fsmoe_gemm_desc& d) {
+    d.precision = cfg.precision == Precision::f32 ? 1 : 0;
+    throw_on(fsmoe_grouped_gemm(&d, s_comp));
+  }
+
+  fsmoe_gemm_desc row_desc(const Chunk& c) const {
+    fsmoe_gemm_desc d{};
+    d.kind = 0;
+    d.nblk = P * El;
+    d.n_w = El;
+    d.rows = c.hi - c.lo;
+    d.rows_total = static_cast<int>(C);
+    d.row0 = c.lo;
+    d.valid_rows = P > 1 ? rfill : fill;
+    return d;
+  }
+
+  fsmoe_gemm_desc k_desc(const Chunk& c, bool accumulate) const {
+    fsmoe_gemm_desc d = row_desc(c);
+    d.kind = 1;
+    d.epi = 1;
+    d.accumulate = accumulate ? 1 : 0;
+    return d;
+  }
+
+  void expert_fwd(const Chunk& c) {
+    const bool bf = cfg.precision == Precision::bf16;
+    const bool gated = cfg.ffn == LayerConfig::Ffn::gated3;
+    // GEMM1: Z = X W1^T (+ fused activation -> H)
+    fsmoe_gemm_desc g1 = row_desc(c);
+    g1.K = M;
+    g1.N = N1;
+    g1.A = Xr;
+    g1.B = prm.w1;
+    g1.D = Z;
+    g1.ldd = N1;
+    if (bf) {
+      g1.epi = gated ? 3 : 2;
+      g1.D2 = Hh;
+      g1.ldd2 = H;
+    } else {
+      g1.epi = 1;
+    }
+    gemm(g1);
+    if (!bf)
+      throw_on(fsmoe_activation_f32(gated ? 3 : 2, P * El, static_cast<int>(C), c.lo, c.hi - c.lo, H,
+                                    static_cast<const float*>(Z), nullptr,
+                                    static_cast<float*>(Hh), s_comp));
+    // GEMM2: O = H W2^T
+    fsmoe_gemm_desc g2 = row_desc(c);
+    g2.K = H;
+    g2.N = M;
+    g2.A = Hh;
+    g2.B = prm.w2;
+    g2.D = Or;
+    g2.ldd = M;
+    g2.epi = bf ? 0 : 1;
+    gemm(g2);
+  }
+
+  void expert_bwd(const Chunk& c, bool first) {
+    const bool bf = cfg.precision == Precision::bf16;
+    const bool gated = cfg.ffn == LayerConfig::Ffn::gated3;
+    // wgrad2: dW2[e] (M x H) += dO^T H
+    fsmoe_gemm_desc w2 = k_desc(c, !first);
+    w2.Mo = M;
+    w2.No = H;
+    w2.A = dOr;
+    w2.B = Hh;
+    w2.D = prm.g_w2;
+    w2.ldd = H;
+    gemm(w2);
+    // dgrad2: dH = dO W2 ; dZ = dH * act'(Z)   (written over Z)
+    fsmoe_gemm_desc d2 = row_desc(c);
+    d2.K = M;
+    d2.N = H;
+    d2.b_mn_major = 1;
+    d2.A = dOr;
+    d2.B = prm.w2;
+    if (bf) {
+      d2.epi = gated ? 5 : 4;
+      d2.Zin = Z;
+      d2.ldz = N1;
+      d2.D = Z;
+      d2.ldd = N1;
+      gemm(d2);
+    } else {
+      d2.epi = 1;
+      d2.D = Hh;  // dH over H (wgrad2 already consumed it)
+      d2.ldd = H;
+      gemm(d2);
+      throw_on(fsmoe_activation_f32(gated ? 5 : 4, P * El, static_cast<int>(C), c.lo, c.hi - c.lo, H,
+                                    static_cast<const float*>(Hh), static_cast<const float*>(Z),
+                                    static_cast<float*>(Z), s_comp));
+    }
+    // wgrad1: dW1[e] (N1 x M) += dZ^T X
+    fsmoe_gemm_desc w1 = k_desc(c, !first);
+    w1.Mo = N1;
+    w1.No = M;
+    w1.A = Z;
+    w1.B = Xr;
+    w1.D = prm.g_w1;
+    w1.ldd = M;
+    gemm(w1);
+    // dgrad1: dX = dZ W1
+    fsmoe_gemm_desc d1 = row_desc(c);
+    d1.K = N1;
+    d1.N = M;
+    d1.b_mn_major = 1;
+    d1.A = Z;
+    d1.B = prm.w1;
+    d1.D = dXr;
+    d1.ldd = M;
+    d1.epi = bf ? 0 : 1;
+    gemm(d1);
+  }
+
+  // ------------------------------------------------------- exchanges --
+  // Send rows [lo,hi) of every block of `send` ([E][C][M], e = p*E_l + e_l)
+  // to rank p, receive rank p's rows into `recv` block (p, e_l).
+  void exchange(const void* send, void* recv, const Chunk& c) {
+    const size_t row = static_cast<size_t>(M) * esz;
+    const size_t n = static_cast<size_t>(c.hi - c.lo) * M;
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int p = 0; p < P; ++p) {
+      for (int el = 0; el < El; ++el) {
+        const size_t blk = static_cast<size_t>(p * El + el);
+        const char* sp = static_cast<const char*>(send) + (blk * C + c.lo) * row;
+        char* rp = static_cast<char*>(recv) + (blk * C + c.lo) * row;
+        nccl_check(ncclSend(sp, n, nccl_dt, p, ep->comm(), s_comm), "ncclSend");
+        nccl_check(ncclRecv(rp, n, nccl_dt, p, ep->comm(), s_comm), "ncclRecv");
+      }
+    }
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  }
+
+  void exchange_fill() {
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int p = 0; p < P; ++p) {
+      nccl_check(ncclSend(fill + static_cast<size_t>(p) * El, El, ncclInt64, p, ep->comm(), s_comm),
+                 "ncclSend");
+      nccl_check(ncclRecv(rfill + static_cast<size_t>(p) * El, El, ncclInt64, p, ep->comm(), s_comm),
+                 "ncclRecv");
+    }
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  }
+
+  void allreduce_slices() {
+    if (!prm.dense_grad || cfg.dense_grad_elems <= 0) return;
+    std::vector<long long> sl = cfg.ar_slices;
+    if (sl.empty()) sl.push_back(cfg.dense_grad_elems);
+    long long off = 0;
+    for (long long n : sl) {
+      n = std::min(n, cfg.dense_grad_elems - off);
+      if (n <= 0) break;
+      nccl_check(ncclAllReduce(prm.dense_grad + off, prm.dense_grad + off, static_cast<size_t>(n),
+                               ncclFloat32, ncclSum, ep->comm(), s_comm),
+                 "ncclAllReduce");
+      off += n;
+    }
+  }
+
+  void record(cudaEvent_t e, cudaStream_t s) { cuda_check(cudaEventRecord(e, s), "eventRecord"); }
+  void wait(cudaStream_t s, cudaEvent_t e) { cuda_check(cudaStreamWaitEvent(s, e, 0), "waitEvent"); }
+};
+
+MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cfg_(cfg) {
+  Impl& I = *impl_;
+  I.cfg = cfg;
+  I.ep = ep;
+  I.P = ep ? ep->world() : 1;
+  I.rank = ep ? ep->rank() : 0;
+  world_ = I.P;
+  if (cfg.tokens <= 0 || cfg.model_dim <= 0 || cfg.ffn_dim <= 0 || cfg.experts <= 0 || cfg.top_k <= 0)
+    throw ConfigError("layer: tokens, model_dim, ffn_dim, experts and top_k must be positive");
+  if (cfg.experts % I.P != 0)
+    throw ConfigError("experts must divide evenly across expert_parallel groups");
+  if (cfg.model_dim % 64 || cfg.ffn_dim % 128)
+    throw ConfigError("layer: model_dim must be a multiple of 64 and ffn_dim of 128");
+  cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+  I.E = cfg.experts;
+  I.El = I.E / I.P;
+  el_ = I.El;
+  I.T = cfg.tokens;
+  I.M = cfg.model_dim;
+  I.H = cfg.ffn_dim;
+  I.k = cfg.top_k;
+  I.N1 = cfg.ffn == LayerConfig::Ffn::gated3 ? 2 * I.H : I.H;
+  if (cfg.capacity > 0) {
+    I.C = cfg.capacity;
+  } else {
+    LayerConfig lc;
+    lc.batch = 1;
+    lc.heads = 1;
+    lc.seq_len = cfg.tokens;
+    lc.model_dim = cfg.model_dim;
+    lc.hidden_scale = 1;
+    lc.capacity_factor = 1.0;
+    lc.experts = cfg.experts;
+    lc.top_k = cfg.top_k;
+    I.C = capacity_tokens(lc);
+  }
+  cap_ = I.C;
+  const bool bf = cfg.precision == Precision::bf16;
+  I.esz = bf ? 2 : 4;
+  I.dtype = bf ? FSMOE_BF16 : FSMOE_F32;
+  I.nccl_dt = bf ? ncclBfloat16 : ncclFloat32;
+  I.fwd_chunks = make_chunks(I.C, cfg.r_fwd);
+  I.bwd_chunks = make_chunks(I.C, cfg.r_bwd);
+
+  // gate descriptor
+  fsmoe_gate_desc& d = I.gd;
+  d.kind = gate_kind_abi(cfg.gate);
+  d.top_k = cfg.gate == GateKind::expert_choice ? static_cast<int>(I.C) : cfg.top_k;
+  d.seed = cfg.seed;
+  d.tokens = I.T;
+  d.model_dim = I.M;
+  d.x_dtype = I.dtype;
+  const bool cosine = cfg.gate == GateKind::cosine_topk;
+  d.score_rows = cosine ? cfg.proj_dim : I.M;
+  d.score_cols = I.E;
+  d.noise_rows = I.M;
+  d.noise_cols = I.E;
+  d.proj_rows = cosine ? cfg.proj_dim : 0;
+  d.proj_cols = cosine ? I.M : 0;
+  throw_on(fsmoe_gate_validate(&d));
+  I.n_picks = cfg.gate == GateKind::expert_choice ? static_cast<long long>(I.E) * d.top_k
+                                                  : static_cast<long long>(I.T) * I.k;
+  if (cfg.gate == GateKind::expert_choice && I.C > I.T)
+    throw ConfigError("gate: expert capacity exceeds token count");
+
+  cuda_check(cudaStreamCreateWithPriority(&I.s_comp, cudaStreamNonBlocking, 0), "stream");
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cuda_check(cudaStreamCreateWithPriority(&I.s_comm, cudaStreamNonBlocking, hi), "stream");
+  for (cudaEvent_t* e : {&I.ev_in, &I.ev_out, &I.ev_gate, &I.ev_join})
+    cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+  const size_t nev = std::max(I.fwd_chunks.size(), I.bwd_chunks.size());
+  I.ev_a.resize(nev);
+  I.ev_b.resize(nev);
+  for (size_t i = 0; i < nev; ++i) {
+    cuda_check(cudaEventCreateWithFlags(&I.ev_a[i], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&I.ev_b[i], cudaEventDisableTiming), "event");
+  }
+
+  const long long P_ = I.n_picks, T = I.T, E = I.E, C = I.C, M = I.M;
+  I.tok = static_cast<int*>(I.dalloc("pick_token", 4 * P_));
+  I.exp = static_cast<int*>(I.dalloc("pick_expert", 4 * P_));
+  I.w = static_cast<double*>(I.dalloc("pick_weight", 8 * P_));
+  I.dw = static_cast<double*>(I.dalloc("d_weight", 8 * P_));
+  I.slot = static_cast<int*>(I.dalloc("slot_of_pick", 4 * P_));
+  I.pos = static_cast<int*>(I.dalloc("pick_of_slot", 4 * E * C));
+  I.tptr = static_cast<int*>(I.dalloc("tok_ptr", 4 * (T + 1)));
+  I.tpick = static_cast<int*>(I.dalloc("tok_pick", 4 * P_));
+  I.status = static_cast<int*>(I.dalloc("status", 8));
+  I.fill = static_cast<long long*>(I.dalloc("fill", 8 * E));
+  I.dropped = static_cast<long long*>(I.dalloc("dropped", 8));
+  I.rfill = I.P > 1 ? static_cast<long long*>(I.dalloc("recv_fill", 8 * E)) : I.fill;
+  I.scores = static_cast<double*>(I.dalloc("scores", 8 * T * E));
+  if (cfg.gate == GateKind::noisy_topk) {
+    I.noise = static_cast<double*>(I.dalloc("noise", 8 * T * E));
+    I.spread = static_cast<double*>(I.dalloc("spread", 8 * T * E));
+  }
+  if (cosine) I.proj_out = static_cast<double*>(I.dalloc("proj_out", 8 * T * cfg.proj_dim));
+  I.gate_wsb = fsmoe_gate_workspace_size(&d);
+  I.gate_ws = I.dalloc("gate_ws", static_cast<long long>(I.gate_wsb));
+  I.assign_wsb = fsmoe_assign_workspace_size(P_, I.E);
+  I.assign_ws = I.dalloc("assign_ws", static_cast<long long>(I.assign_wsb));
+  I.tidx_wsb = fsmoe_token_index_workspace_size(P_, I.T);
+  I.tidx_ws = I.dalloc("tidx_ws", static_cast<long long>(I.tidx_wsb));
+  I.gbwd_wsb = fsmoe_gate_bwd_workspace_size(&d);
+  I.gbwd_ws = I.dalloc("gate_bwd_ws", static_cast<long long>(I.gbwd_wsb));
+
+  const long long rows = E * C;  // == P * E_l * C on both sides
+  const long long ab = rows * M * I.esz;
+  I.Xs = I.dalloc("X_send", ab);
+  I.Xr = I.P > 1 ? I.dalloc("X_recv", ab) : I.Xs;
+  if (I.P == 1) I.alias("X_recv", I.Xr, ab);
+  I.Z = I.dalloc("Z", rows * I.N1 * I.esz);
+  I.Hh = I.dalloc("H", rows * I.H * I.esz);
+  I.Or = I.dalloc("O_recv", ab);
+  I.Os = I.P > 1 ? I.dalloc("O_send", ab) : I.Or;
+  if (I.P == 1) I.alias("O_send", I.Os, ab);
+  I.dOs = I.dalloc("dO_send", ab);
+  I.dOr = I.P > 1 ? I.dalloc("dO_recv", ab) : I.dOs;
+  I.dXr = I.dalloc("dX_recv", ab);
+  I.dXs = I.P > 1 ? I.dalloc("dX_send", ab) : I.dXr;
+  cuda_check(cudaMemsetAsync(I.status, 0, 8, I.s_comp), "memset");
+  cuda_check(cudaStreamSynchronize(I.s_comp), "sync");
+}
+
+MoELayer::~MoELayer() = default;
+
+void MoELayer::bind(const MoEParams& p) {
+  if (!p.w_gate || !p.w1 || !p.w2 || !p.g_w1 || !p.g_w2 || !p.g_gate)
+    throw ConfigError("layer: bind needs w_gate, w1, w2 and their gradients");
+  if (cfg_.gate == GateKind::noisy_topk && (!p.w_noise || !p.g_noise))
+    throw ConfigError("layer: noisy_topk needs w_noise and g_noise");
+  if (cfg_.gate == GateKind::cosine_topk && (!p.proj || !p.g_proj))
+    throw ConfigError("layer: cosine_topk needs proj and g_proj");
+  impl_->prm = p;
+}
+
+void MoELayer::forward(const void* x, void* y, void* stream) {
+  Impl& I = *impl_;
+  cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  I.record(I.ev_in, st);
+  I.wait(I.s_comp, I.ev_in);
+  I.x_last = x;
+  // K1 gate, K2 assign, token index, K3 dispatch
+  throw_on(fsmoe_gate(&I.gd, x, I.prm.w_gate, I.prm.w_noise, I.prm.proj, I.tok, I.exp, I.w,
+                      I.scores, I.noise, I.spread, I.proj_out, I.status, I.gate_ws, I.gate_wsb,
+                      I.s_comp));
+  throw_on(fsmoe_assign(I.n_picks, I.tok, I.exp, I.T, I.E, I.C, I.slot, I.fill, I.dropped, I.pos,
+                        I.status, I.assign_ws, I.assign_wsb, I.s_comp));
+  const int kmajor = cfg_.gate == GateKind::expert_choice ? 0 : I.k;
+  throw_on(fsmoe_token_index(I.n_picks, I.tok, I.T, kmajor, I.tptr, I.tpick, I.tidx_ws,
+                             I.tidx_wsb, I.s_comp));
+  throw_on(fsmoe_dispatch(I.dtype, I.M, I.E, I.C, 1, I.pos, I.tok, x, I.Xs, I.s_comp));
+  const auto& ch = I.fwd_chunks;
+  if (I.P > 1) {
+    I.record(I.ev_gate, I.s_comp);
+    I.wait(I.s_comm, I.ev_gate);
+    I.exchange_fill();
+    for (size_t i = 0; i < ch.size(); ++i) {
+      I.exchange(I.Xs, I.Xr, ch[i]);
+      I.record(I.ev_a[i], I.s_comm);
+    }
+  }
+  for (size_t i = 0; i < ch.size(); ++i) {
+    if (I.P > 1) I.wait(I.s_comp, I.ev_a[i]);
+    I.expert_fwd(ch[i]);
+    if (I.P > 1) I.record(I.ev_b[i], I.s_comp);
+  }
+  if (I.P > 1) {
+    for (size_t i = 0; i < ch.size(); ++i) {
+      I.wait(I.s_comm, I.ev_b[i]);
+      I.exchange(I.Or, I.Os, ch[i]);
+    }
+    I.record(I.ev_join, I.s_comm);
+    I.wait(I.s_comp, I.ev_join);
+  }
+  // K5 combine
+  throw_on(fsmoe_combine(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.w, I.Os, y,
+                         I.s_comp));
+  I.record(I.ev_out, I.s_comp);
+  I.wait(st, I.ev_out);
+}
+
+void MoELayer::backward(const void* dy, void* dx, void* stream) {
+  Impl& I = *impl_;
+  cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  I.record(I.ev_in, st);
+  I.wait(I.s_comp, I.ev_in);
+  const MoEParams& p = I.prm;
+  // gate gradients accumulate inside gate_bwd: start from zero
+  const long long ge = static_cast<long long>(I.gd.score_rows) * I.E;
+  cuda_check(cudaMemsetAsync(p.g_gate, 0, 8 * ge, I.s_comp), "memset");
+  if (p.g_noise) cuda_check(cudaMemsetAsync(p.g_noise, 0, 8LL * I.M * I.E, I.s_comp), "memset");
+  if (p.g_proj)
+    cuda_check(cudaMemsetAsync(p.g_proj, 0, 8LL * cfg_.proj_dim * I.M, I.s_comp), "memset");
+  // I-order backward: dO (send side) and d weights
+  throw_on(fsmoe_combine_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.n_picks, I.pos, I.tok, I.w, I.slot,
+                             dy, I.Os, I.dOs, I.dw, I.s_comp));
+  const auto& ch = I.bwd_chunks;
+  if (I.P > 1) {
+    I.record(I.ev_gate, I.s_comp);
+    I.wait(I.s_comm, I.ev_gate);
+    for (size_t j = 0; j < ch.size(); ++j) {
+      I.exchange(I.dOs, I.dOr, ch[j]);
+      I.record(I.ev_a[j], I.s_comm);
+    }
+    // gradient allreduce slices between the last dispatch and the first combine
+    I.allreduce_slices();
+  }
+  for (size_t j = 0; j < ch.size(); ++j) {
+    if (I.P > 1) I.wait(I.s_comp, I.ev_a[j]);
+    I.expert_bwd(ch[j], j == 0);
+    if (I.P > 1) I.record(I.ev_b[j], I.s_comp);
+  }
+  if (I.P > 1) {
+    for (size_t j = 0; j < ch.size(); ++j) {
+      I.wait(I.s_comm, I.ev_b[j]);
+      I.exchange(I.dXr, I.dXs, ch[j]);
+    }
+    I.record(I.ev_join, I.s_comm);
+    I.wait(I.s_comp, I.ev_join);
+  }
+  // Order backward, then the gate's contribution to dx and its parameters
+  throw_on(fsmoe_dispatch_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.dXs, dx,
+                              0, I.s_comp));
+  if (!I.x_last) throw ConfigError("layer: backward before forward");
+  throw_on(fsmoe_gate_bwd(&I.gd, I.x_last, p.w_gate, p.w_noise, p.proj,
+                          I.tok, I.exp, I.w, I.dw, I.scores, I.noise, I.spread, I.proj_out, dx,
+                          p.g_gate, p.g_noise, p.g_proj, I.gbwd_ws, I.gbwd_wsb, I.s_comp));
+  if (I.P > 1) {
+    // replicated gate parameters: sum their gradients over the EP group
+    I.record(I.ev_gate, I.s_comp);
+    I.wait(I.s_comm, I.ev_gate);
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    nccl_check(ncclAllReduce(p.g_gate, p.g_gate, ge, ncclFloat64, ncclSum, I.ep->comm(), I.s_comm),
+               "ncclAllReduce");
+    if (p.g_noise)
+      nccl_check(ncclAllReduce(p.g_noise, p.g_noise, static_cast<size_t>(I.M) * I.E, ncclFloat64,
+                               ncclSum, I.ep->comm(), I.s_comm),
+                 "ncclAllReduce");
+    if (p.g_proj)
+      nccl_check(ncclAllReduce(p.g_proj, p.g_proj, static_cast<size_t>(cfg_.proj_dim) * I.M,
+                               ncclFloat64, ncclSum, I.ep->comm(), I.s_comm),
+                 "ncclAllReduce");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    I.record(I.ev_join, I.s_comm);
+    I.wait(I.s_comp, I.ev_join);
+  }
+  I.record(I.ev_out, I.s_comp);
+  I.wait(st, I.ev_out);
+}
+
+void* MoELayer::buffer(const std::string& name, long long* bytes) const {
+  auto it = impl_->bufs.find(name);
+  if (it == impl_->bufs.end()) throw ConfigError("layer: unknown buffer " + name);
+  if (bytes) *bytes = it->second.second;
+  return it->second.first;
+}
+
+long long MoELayer::dropped_host() const {
+  long long h = 0;
+  cuda_check(cudaMemcpyAsync(&h, impl_->dropped, 8, cudaMemcpyDeviceToHost, impl_->s_comp), "copy");
+  cuda_check(cudaStreamSynchronize(impl_->s_comp), "sync");
+  return h;
+}
+
+}  // namespace fsmoe

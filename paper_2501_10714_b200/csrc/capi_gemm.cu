@@ -29,14 +29,20 @@ int cuda_status(cudaError_t e, const char* where) {
 
 namespace {
 
-__global__ void act_f32_kernel(int op, long long rows, int units, const float* __restrict__ in,
-                               const float* __restrict__ z, float* __restrict__ out,
-                               float* __restrict__ out2) {
-  long long n = rows * units;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    long long r = i / units;
-    int u = static_cast<int>(i - r * units);
+__global__ void act_f32_kernel(int op, int nblk, int rows_total, int row0, int rows, int units,
+                               const float* __restrict__ in0, const float* __restrict__ z0,
+                               float* __restrict__ out0) {
+  long long n = static_cast<long long>(nblk) * rows * units;
+  for (long long li = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; li < n;
+       li += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long lr = li / units;
+    int u = static_cast<int>(li - lr * units);
+    long long b = lr / rows;
+    long long r = b * rows_total + row0 + (lr - b * rows);  // absolute row
+    long long i = r * units + u;
+    const float* in = in0;
+    const float* z = z0;
+    float* out = out0;
     int gcol = (u / 128) * 256 + (u % 128);  // interleaved gate/up column of unit u
     switch (op) {
       case 2: {  // gelu fwd: in = Z (rows x units) -> out = gelu(Z)
@@ -82,6 +88,17 @@ const char* fsmoe_last_error(void) { return fsmoe::g_last_error.c_str(); }
 
 int fsmoe_abi_version(void) { return 1; }
 
+int fsmoe_copy_device(void* dst, const void* src, size_t bytes, void* stream) {
+  FSMOE_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, fsmoe::as_stream(stream)),
+                 "fsmoe_copy_device");
+  return FSMOE_OK;
+}
+
+int fsmoe_set_device(int device) {
+  FSMOE_CUDA_TRY(cudaSetDevice(device), "fsmoe_set_device");
+  return FSMOE_OK;
+}
+
 int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   using namespace fsmoe;
   if (!d) return config_error("gemm: null descriptor");
@@ -94,6 +111,8 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   p.Mo = d->Mo;
   p.No = d->No;
   p.n_w = d->n_w;
+  p.rows_total = d->rows_total;
+  p.row0 = d->row0;
   p.b_mn_major = d->b_mn_major != 0;
   p.A = d->A;
   p.B = d->B;
@@ -115,15 +134,17 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   return cuda_status(static_cast<cudaError_t>(rc), "fsmoe_grouped_gemm");
 }
 
-int fsmoe_activation_f32(int op, long long rows, int units, const float* in, const float* z,
-                         float* out, float* out2, void* stream) {
+int fsmoe_activation_f32(int op, int nblk, int rows_total, int row0, int rows, int units,
+                         const float* in, const float* z, float* out, void* stream) {
   using namespace fsmoe;
   if (op < 2 || op > 5) return config_error("activation: unknown op");
-  if (rows <= 0 || units <= 0) return FSMOE_OK;
+  if (nblk <= 0 || rows <= 0 || units <= 0) return FSMOE_OK;
+  if (row0 < 0 || row0 + rows > rows_total) return config_error("activation: bad row window");
   if ((op == 3 || op == 5) && units % 128) return config_error("activation: swiglu units % 128");
-  long long n = rows * units;
+  long long n = static_cast<long long>(nblk) * rows * units;
   int grid = static_cast<int>((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
-  act_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(op, rows, units, in, z, out, out2);
+  act_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(op, nblk, rows_total, row0, rows, units, in,
+                                                      z, out);
   return cuda_status(cudaGetLastError(), "fsmoe_activation_f32");
 }
 

@@ -16,9 +16,15 @@
 //    B: [nblk][rows][No] (No contiguous) -> MN-major operand
 //    D: [E_w][Mo][No] fp32, optionally accumulated (pipeline chunks).
 //
+// Row window: every block holds `rows_total` rows in memory (the capacity C);
+// one launch processes rows [row0, row0 + rows) of each block (a pipeline
+// chunk). Row-grouped outputs (and Zin / D2) use the same [nblk][rows_total]
+// row addressing. row0 must be a multiple of 128 unless rows reaches the end.
+//
 // `valid_rows[b]` (optional, device int64 per block) is the dispatch fill of
-// that block: row tiles entirely past it are skipped (their rows are capacity
-// padding) and wgrad's K extent stops at round_up(valid, 64).
+// that block (absolute row count): row tiles entirely past it are skipped
+// (their rows are capacity padding) and wgrad's K extent stops at
+// round_up(valid, 64).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -39,7 +45,9 @@ enum class Epi : int {
 struct GemmProblem {
   GemmKind kind = GemmKind::RowGrouped;
   int nblk = 0;        // A/B blocks (row-grouped: output blocks too)
-  int rows = 0;        // rows per block
+  int rows = 0;        // rows per block processed by this launch
+  int rows_total = 0;  // rows per block in memory (0 -> rows)
+  int row0 = 0;        // first processed row of each block
   int K = 0;           // row-grouped reduction dim
   int N = 0;           // row-grouped output columns
   int Mo = 0, No = 0;  // k-grouped output dims

@@ -12,7 +12,7 @@ namespace {
 constexpr int TM = 64, TN = 64, TK = 16;
 
 struct SParams {
-  int kind, nblk, rows, K, N, Mo, No, n_w, b_mn;
+  int kind, nblk, rows, K, N, Mo, No, n_w, b_mn, rows_total, row0;
   const long long* valid;
   const float* A;
   const float* B;
@@ -23,7 +23,7 @@ struct SParams {
 
 __device__ __forceinline__ int valid_rows(const SParams& p, int b) {
   if (!p.valid) return p.rows;
-  long long v = p.valid[b];
+  long long v = p.valid[b] - p.row0;
   return v < 0 ? 0 : (v > p.rows ? p.rows : static_cast<int>(v));
 }
 
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SParams p) {
 
   if (p.kind == 0) {
     const int w = g % p.n_w;
-    const float* A = p.A + static_cast<long long>(g) * p.rows * p.K;
+    const float* A = p.A + (static_cast<long long>(g) * p.rows_total + p.row0) * p.K;
     auto la = [&](int r, int k) -> float {
       return (r < p.rows && k < p.K) ? A[static_cast<long long>(r) * p.K + k] : 0.f;
     };
@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SParams p) {
   } else {
     for (int b = g; b < p.nblk; b += p.n_w) {
       const int vr = valid_rows(p, b);
-      const float* A = p.A + static_cast<long long>(b) * p.rows * p.Mo;
-      const float* B = p.B + static_cast<long long>(b) * p.rows * p.No;
+      const float* A = p.A + (static_cast<long long>(b) * p.rows_total + p.row0) * p.Mo;
+      const float* B = p.B + (static_cast<long long>(b) * p.rows_total + p.row0) * p.No;
       auto la = [&](int m, int r) -> float {
         return (m < p.Mo && r < vr) ? A[static_cast<long long>(r) * p.Mo + m] : 0.f;
       };
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SParams p) {
     }
   }
 
-  const long long gstride = static_cast<long long>(out_rows) * p.ldd;
+
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int r = m0 + ty * 4 + i;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SParams p) {
     for (int j = 0; j < 4; ++j) {
       int c = n0 + tx * 4 + j;
       if (c >= out_cols) continue;
-      float* d = p.D + g * gstride + static_cast<long long>(r) * p.ldd + c;
+      float* d = p.D + (p.kind == 0 ? (static_cast<long long>(g) * p.rows_total + p.row0 + r) : (static_cast<long long>(g) * p.Mo + r)) * p.ldd + c;
       *d = p.accumulate ? *d + acc[i][j] : acc[i][j];
     }
   }
@@ -117,6 +117,9 @@ int gemm_simt_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.kind = static_cast<int>(pr.kind);
   p.nblk = pr.nblk;
   p.rows = pr.rows;
+  p.rows_total = pr.rows_total > 0 ? pr.rows_total : pr.rows;
+  p.row0 = pr.row0;
+  if (p.row0 < 0 || p.row0 + p.rows > p.rows_total) return cudaErrorInvalidValue;
   p.K = pr.K;
   p.N = pr.N;
   p.Mo = pr.Mo;

@@ -48,16 +48,17 @@ struct KParams {
   void* D2;
   const void* Zin;
   long long ldd, ldd2, ldz;
-  long long d_gstride;  // elements between output groups
+  int rows_total, row0;  // block row window (see gemm.h)
   int accumulate;
   int out_rows, out_cols;  // valid output extent per group
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// Valid rows of block b inside the processed window [row0, row0 + rows).
 __device__ __forceinline__ int valid_of(const KParams& p, int b) {
   if (!p.valid) return p.rows;
-  long long v = p.valid[b];
+  long long v = p.valid[b] - p.row0;
   return v < 0 ? 0 : (v > p.rows ? p.rows : static_cast<int>(v));
 }
 
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint8_t* sa = smem + s * STAGE_BYTES;
             uint8_t* sb = sa + A_STAGE_BYTES;
             mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
-            tma_load_3d(sa, &tmA, &full_bar[s], kb * BK, ti.mt * BM, ti.g);
+            tma_load_3d(sa, &tmA, &full_bar[s], kb * BK, p.row0 + ti.mt * BM, ti.g);
             if (!b_mn) {
               tma_load_3d(sb, &tmB, &full_bar[s], kb * BK, ti.nt * BN, w);
             } else {
@@ -200,10 +201,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
 #pragma unroll
               for (int i = 0; i < BM / 64; ++i)
-                tma_load_3d(sa + i * 8192, &tmA, &full_bar[s], ti.mt * BM + i * 64, kb * BK, b);
+                tma_load_3d(sa + i * 8192, &tmA, &full_bar[s], ti.mt * BM + i * 64, p.row0 + kb * BK, b);
 #pragma unroll
               for (int i = 0; i < BN / 64; ++i)
-                tma_load_3d(sb + i * 8192, &tmB, &full_bar[s], ti.nt * BN + i * 64, kb * BK, b);
+                tma_load_3d(sb + i * 8192, &tmB, &full_bar[s], ti.nt * BN + i * 64, p.row0 + kb * BK, b);
               if (++s == STAGES) { s = 0; ph ^= 1; }
             }
           }
@@ -262,16 +263,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int nkb = total_kblocks(p, ti.g);
       mbar_wait(&tfull_bar[acc], aph);
       tc_fence_after();
-      const int row = ti.mt * BM + q * 32 + lane;
+      const int row = ti.mt * BM + q * 32 + lane;  // within the processed window
       const bool row_ok = row < p.out_rows;
+      const long long orow = p.kind == 0
+                                 ? static_cast<long long>(ti.g) * p.rows_total + p.row0 + row
+                                 : static_cast<long long>(ti.g) * p.Mo + row;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       uint32_t r[32];
       float v[32];
       if (p.epi == static_cast<int>(Epi::SwigluFwd)) {
         // tile cols: [0,128) gate units, [128,256) up units (same 128 units)
-        __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + ti.g * p.d_gstride + row * p.ldd;
+        __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
         __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) +
-                           static_cast<long long>(ti.g) * p.rows * p.ldd2 + row * p.ldd2;
+                           orow * p.ldd2;
         for (int c = 0; c < 4; ++c) {
           float g[32];
           if (nkb > 0) {
@@ -317,12 +321,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (!row_ok || col >= p.out_cols) continue;
           switch (p.epi) {
             case static_cast<int>(Epi::StoreBF16): {
-              __nv_bfloat16* D = static_cast<__nv_bfloat16*>(p.D) + ti.g * p.d_gstride + row * p.ldd;
+              __nv_bfloat16* D = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
               store_bf16x32(D + col, v);
               break;
             }
             case static_cast<int>(Epi::StoreF32): {
-              float* D = static_cast<float*>(p.D) + ti.g * p.d_gstride + row * p.ldd + col;
+              float* D = static_cast<float*>(p.D) + orow * p.ldd + col;
               float4* d4 = reinterpret_cast<float4*>(D);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -336,9 +340,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               break;
             }
             case static_cast<int>(Epi::GeluFwd): {
-              __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + ti.g * p.d_gstride + row * p.ldd;
+              __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
               __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) +
-                                 static_cast<long long>(ti.g) * p.rows * p.ldd2 + row * p.ldd2;
+                                 orow * p.ldd2;
               store_bf16x32(Z + col, v);
               float h[32];
 #pragma unroll
@@ -348,8 +352,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             case static_cast<int>(Epi::GeluBwd): {
               const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) +
-                                       static_cast<long long>(ti.g) * p.rows * p.ldz + row * p.ldz;
-              __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + ti.g * p.d_gstride + row * p.ldd;
+                                       orow * p.ldz;
+              __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
               float z[32];
               load_bf16x32(Z + col, z);
 #pragma unroll
@@ -361,8 +365,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int unit = col;
               const int gcol = (unit / 128) * 256 + (unit % 128);
               const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) +
-                                       static_cast<long long>(ti.g) * p.rows * p.ldz + row * p.ldz;
-              __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + ti.g * p.d_gstride + row * p.ldd;
+                                       orow * p.ldz;
+              __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
               float g[32], u[32], dg[32];
               load_bf16x32(Z + gcol, g);
               load_bf16x32(Z + gcol + 128, u);
@@ -461,7 +465,12 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.ldd2 = pr.ldd2;
   p.ldz = pr.ldz;
   p.accumulate = pr.accumulate ? 1 : 0;
+  p.rows_total = pr.rows_total > 0 ? pr.rows_total : pr.rows;
+  p.row0 = pr.row0;
   if (pr.nblk <= 0 || pr.rows <= 0) return cudaSuccess;
+  if (p.row0 < 0 || p.row0 + pr.rows > p.rows_total || p.row0 % 64) return cudaErrorInvalidValue;
+  if (pr.kind == GemmKind::KGrouped && p.row0 + pr.rows < p.rows_total && pr.rows % 64)
+    return cudaErrorInvalidValue;  // the K window must end on a 64-row boundary
   if (pr.kind == GemmKind::RowGrouped) {
     if (pr.K % 8 || pr.N % 64 || pr.K <= 0 || pr.N <= 0) return cudaErrorInvalidValue;
     p.m_tiles = (pr.rows + BM - 1) / BM;
@@ -470,8 +479,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     p.out_rows = pr.rows;
     // SwigluBwd's output columns are the interleaved dZ (2N); masking is on N units.
     p.out_cols = pr.N;
-    p.d_gstride = static_cast<long long>(pr.rows) * pr.ldd;
-    if (!make_map3(&ta, pr.A, pr.K, pr.rows, pr.nblk, BK, BM)) return cudaErrorInvalidValue;
+    if (!make_map3(&ta, pr.A, pr.K, p.rows_total, pr.nblk, BK, BM)) return cudaErrorInvalidValue;
     if (!pr.b_mn_major) {
       if (!make_map3(&tb, pr.B, pr.K, pr.N, p.n_w, BK, BN)) return cudaErrorInvalidValue;
     } else {
@@ -484,9 +492,8 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     p.n_groups = p.n_w;
     p.out_rows = pr.Mo;
     p.out_cols = pr.No;
-    p.d_gstride = static_cast<long long>(pr.Mo) * pr.ldd;
-    if (!make_map3(&ta, pr.A, pr.Mo, pr.rows, pr.nblk, 64, BK)) return cudaErrorInvalidValue;
-    if (!make_map3(&tb, pr.B, pr.No, pr.rows, pr.nblk, 64, BK)) return cudaErrorInvalidValue;
+    if (!make_map3(&ta, pr.A, pr.Mo, p.rows_total, pr.nblk, 64, BK)) return cudaErrorInvalidValue;
+    if (!make_map3(&tb, pr.B, pr.No, p.rows_total, pr.nblk, 64, BK)) return cudaErrorInvalidValue;
   }
   p.num_tiles = p.n_groups * p.m_tiles * p.n_tiles;
   static bool attr_set = false;

@@ -1,0 +1,206 @@
+"""Python handle on the C++ MoE layer (libfsmoe.so, include/fsmoe_layer.h).
+
+Torch allocates the parameters, gradients and activations (device memory and
+streams are the only things torch provides); every FLOP of forward and
+backward happens in the C++ executor and the sm_100a kernels behind it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as NL
+
+GATE_KINDS = {"noisy_topk": 0, "sigmoid_topk": 1, "cosine_topk": 2, "expert_choice": 3}
+FFN_KINDS = {"simple": 0, "gated3": 1}
+
+
+class LayerConfigC(C.Structure):
+    _fields_ = [
+        ("tokens", C.c_int), ("model_dim", C.c_int), ("ffn_dim", C.c_int), ("experts", C.c_int),
+        ("top_k", C.c_int), ("gate_kind", C.c_int), ("ffn_kind", C.c_int),
+        ("capacity", C.c_longlong), ("proj_dim", C.c_int), ("seed", C.c_uint64),
+        ("precision", C.c_int), ("r_fwd", C.c_int), ("r_bwd", C.c_int), ("device", C.c_int),
+        ("dense_grad_elems", C.c_longlong), ("n_ar_slices", C.c_int),
+        ("ar_slices", C.POINTER(C.c_longlong)),
+    ]
+
+
+class LayerParamsC(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("w_gate", "w_noise", "proj", "w1", "w2", "g_gate",
+                                          "g_noise", "g_proj", "g_w1", "g_w2", "dense_grad")]
+
+
+@dataclass
+class MoEConfig:
+    tokens: int
+    model_dim: int
+    ffn_dim: int
+    experts: int
+    top_k: int = 1
+    gate: str = "noisy_topk"
+    ffn: str = "simple"
+    capacity: int = 0            # 0 -> capacity_tokens(k, f=1)
+    capacity_factor: float = 1.0
+    proj_dim: int = 0
+    seed: int = 7
+    precision: str = "bf16"      # or "f32" (check mode)
+    r_fwd: int = 1
+    r_bwd: int = 1
+    dense_grad_elems: int = 0
+    ar_slices: list = field(default_factory=list)
+
+    def resolved_capacity(self) -> int:
+        """capacity_tokens (workload.cpp:43-51) with B*L = tokens."""
+        if self.capacity:
+            return self.capacity
+        if self.gate == "expert_choice":
+            k = self.top_k
+        else:
+            k = self.top_k
+        v = k * self.capacity_factor * self.tokens / self.experts
+        return int(math.ceil(v - 1e-9))
+
+
+class EpGroup:
+    """NCCL expert-parallel communicator owned by libfsmoe.so; torch.distributed
+    only broadcasts the 128-byte unique id."""
+
+    def __init__(self, world: int, rank: int, device: int, max_ctas: int = 0):
+        import torch.distributed as dist
+        lib = NL.cpp_lib()
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            NL.check(lib.fsmoe_ep_unique_id(uid), lib)
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+        if dist.is_initialized() and world > 1:
+            obj = [t]
+            dist.broadcast_object_list(obj, src=0)
+            t = obj[0]
+        uid = (C.c_ubyte * 128)(*t.tolist())
+        h = C.c_void_p()
+        NL.check(lib.fsmoe_ep_create(world, rank, uid, device, max_ctas, C.byref(h)), lib)
+        self.h = h
+        self.world, self.rank = world, rank
+
+    def close(self):
+        if self.h:
+            NL.cpp_lib().fsmoe_ep_destroy(self.h)
+            self.h = None
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class MoELayer:
+    """One FSMoE MoE layer on the current CUDA device (EP over `ep`)."""
+
+    def __init__(self, cfg: MoEConfig, ep: EpGroup | None = None, device=None, init_seed=0):
+        self.cfg = cfg
+        self.ep = ep
+        self.world = ep.world if ep else 1
+        self.rank = ep.rank if ep else 0
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.device = dev
+        assert cfg.experts % self.world == 0
+        self.el = cfg.experts // self.world
+        self.n1 = 2 * cfg.ffn_dim if cfg.ffn == "gated3" else cfg.ffn_dim
+        self.act_dtype = torch.bfloat16 if cfg.precision == "bf16" else torch.float32
+        M, H, E = cfg.model_dim, cfg.ffn_dim, cfg.experts
+        g = torch.Generator(device="cpu").manual_seed(init_seed)
+        rows = cfg.proj_dim if cfg.gate == "cosine_topk" else M
+        # replicated gate parameters (same on every rank): fp64 master copies
+        self.w_gate = ((torch.rand(rows, E, generator=g, dtype=torch.float64) * 2 - 1) / math.sqrt(rows)).to(dev)
+        self.w_noise = ((torch.rand(M, E, generator=g, dtype=torch.float64) * 2 - 1) / math.sqrt(M)).to(dev)
+        self.proj = None
+        if cfg.gate == "cosine_topk":
+            self.proj = ((torch.rand(cfg.proj_dim, M, generator=g, dtype=torch.float64) * 2 - 1)
+                         / math.sqrt(M)).to(dev)
+        # rank-local experts (different stream per rank)
+        ge = torch.Generator(device="cpu").manual_seed(init_seed * 1000 + 17 + self.rank)
+        self.w1 = ((torch.rand(self.el, self.n1, M, generator=ge) * 2 - 1) / math.sqrt(M)).to(dev, self.act_dtype)
+        self.w2 = ((torch.rand(self.el, M, H, generator=ge) * 2 - 1) / math.sqrt(H)).to(dev, self.act_dtype)
+        self.g_gate = torch.zeros_like(self.w_gate)
+        self.g_noise = torch.zeros_like(self.w_noise)
+        self.g_proj = torch.zeros_like(self.proj) if self.proj is not None else None
+        self.g_w1 = torch.zeros(self.el, self.n1, M, device=dev)
+        self.g_w2 = torch.zeros(self.el, M, H, device=dev)
+        self.dense_grad = (torch.zeros(cfg.dense_grad_elems, device=dev)
+                           if cfg.dense_grad_elems else None)
+
+        lib = NL.cpp_lib()
+        c = LayerConfigC()
+        c.tokens, c.model_dim, c.ffn_dim, c.experts = cfg.tokens, M, H, E
+        c.top_k = cfg.top_k
+        c.gate_kind = GATE_KINDS[cfg.gate]
+        c.ffn_kind = FFN_KINDS[cfg.ffn]
+        c.capacity = cfg.resolved_capacity()
+        c.proj_dim = cfg.proj_dim
+        c.seed = cfg.seed
+        c.precision = 0 if cfg.precision == "bf16" else 1
+        c.r_fwd, c.r_bwd = cfg.r_fwd, cfg.r_bwd
+        c.device = dev.index
+        c.dense_grad_elems = cfg.dense_grad_elems
+        self._slices = (C.c_longlong * max(len(cfg.ar_slices), 1))(*cfg.ar_slices)
+        c.n_ar_slices = len(cfg.ar_slices)
+        c.ar_slices = C.cast(self._slices, C.POINTER(C.c_longlong))
+        h = C.c_void_p()
+        NL.check(lib.fsmoe_layer_create(C.byref(c), ep.h if ep else None, C.byref(h)), lib)
+        self.h = h
+        lib.fsmoe_layer_capacity.restype = C.c_longlong
+        self.capacity = lib.fsmoe_layer_capacity(h)
+        self.bind()
+
+    def bind(self):
+        lib = NL.cpp_lib()
+        p = LayerParamsC()
+        p.w_gate, p.w_noise, p.proj = _p(self.w_gate), _p(self.w_noise), _p(self.proj)
+        p.w1, p.w2 = _p(self.w1), _p(self.w2)
+        p.g_gate, p.g_noise, p.g_proj = _p(self.g_gate), _p(self.g_noise), _p(self.g_proj)
+        p.g_w1, p.g_w2, p.dense_grad = _p(self.g_w1), _p(self.g_w2), _p(self.dense_grad)
+        NL.check(lib.fsmoe_layer_bind(self.h, C.byref(p)), lib)
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def forward(self, x, y=None):
+        assert x.is_cuda and x.dtype == self.act_dtype and x.shape == (self.cfg.tokens, self.cfg.model_dim)
+        if y is None:
+            y = torch.empty_like(x)
+        lib = NL.cpp_lib()
+        NL.check(lib.fsmoe_layer_forward(self.h, _p(x), _p(y), self._stream()), lib)
+        return y
+
+    def backward(self, dy, dx=None):
+        if dx is None:
+            dx = torch.empty_like(dy)
+        lib = NL.cpp_lib()
+        NL.check(lib.fsmoe_layer_backward(self.h, _p(dy), _p(dx), self._stream()), lib)
+        return dx
+
+    def buffer(self, name, dtype, shape=None):
+        """View of a named internal device buffer (tests / inspection)."""
+        lib = NL.cpp_lib()
+        ptr, nbytes = C.c_void_p(), C.c_longlong()
+        NL.check(lib.fsmoe_layer_buffer(self.h, name.encode(), C.byref(ptr), C.byref(nbytes)), lib)
+        n = nbytes.value // torch.tensor([], dtype=dtype).element_size()
+        out = torch.empty(n, dtype=dtype, device=self.device)
+        if n:
+            NL.check(NL.cuda_lib().fsmoe_copy_device(_p(out), ptr, C.c_size_t(nbytes.value),
+                                                     self._stream()))
+        return out if shape is None else out.view(shape)
+
+    def close(self):
+        if self.h:
+            NL.cpp_lib().fsmoe_layer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

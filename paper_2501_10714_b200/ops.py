@@ -30,13 +30,14 @@ def _stream():
 
 
 def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn_major=False,
-                 valid_rows=None, epi="store_bf16", D2=None, Zin=None, ldd=None, ldd2=0, ldz=0,
+                 rows_total=0, row0=0, valid_rows=None, epi="store_bf16", D2=None, Zin=None, ldd=None, ldd2=0, ldz=0,
                  accumulate=False, precision=0):
     """Grouped expert GEMM (see csrc/gemm.h). kind: 'row' or 'k'."""
     lib = NL.cuda_lib()
     d = NL.GemmDesc()
     d.kind = 0 if kind == "row" else 1
     d.nblk, d.rows, d.K, d.N, d.Mo, d.No, d.n_w = nblk, rows, K, N, Mo, No, n_w
+    d.rows_total, d.row0 = rows_total, row0
     d.b_mn_major = int(b_mn_major)
     d.A, d.B = _ptr(A), _ptr(B)
     d.valid_rows = _ptr(valid_rows)
@@ -50,10 +51,10 @@ def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn
     NL.check(lib.fsmoe_grouped_gemm(C.byref(d), _stream()))
 
 
-def activation_f32(op, rows, units, inp, z, out, out2=None):
+def activation_f32(op, nblk, rows_total, row0, rows, units, inp, z, out):
     lib = NL.cuda_lib()
-    NL.check(lib.fsmoe_activation_f32(EPI[op], C.c_longlong(rows), units, _ptr(inp), _ptr(z),
-                                     _ptr(out), _ptr(out2), _stream()))
+    NL.check(lib.fsmoe_activation_f32(EPI[op], nblk, rows_total, row0, rows, units, _ptr(inp),
+                                     _ptr(z), _ptr(out), _stream()))
 
 
 # ----------------------------------------------------------------- routing --

@@ -1,0 +1,102 @@
+"""Full MoE layer forward + backward on the GPU (C++ executor, libfsmoe.so)
+against the fp64 restatement (oracle/layer_oracle.py): routing through the C
+port of the reference (bit-exact), FFN + backward per SURVEY.md Appendix D
+(parity unpinned by the reference, which has neither).
+
+Tolerances (max |gpu - ref| / max |ref| per tensor):
+  fp32 check mode (SIMT fp32 GEMMs):        1e-4
+  bf16 mode (tcgen05, bf16 activations):    3e-2 (bf16 rounding of X, Z, H, O, dO, dZ)
+Routing indices / slots / drops: bit-exact in both modes.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    a = a.detach().double().cpu().numpy() if torch.is_tensor(a) else a
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def _run(gate, ffn, precision, T=512, M=256, H=256, E=8, k=2, proj_dim=16, cap=None, r=1,
+         seed=3):
+    from paper_2501_10714_b200.layer import MoEConfig, MoELayer
+    import layer_oracle
+    import pyoracle
+    cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=k, gate=gate, ffn=ffn,
+                    precision=precision, proj_dim=proj_dim if gate == "cosine_topk" else 0,
+                    capacity=cap or 0, seed=11, r_fwd=r, r_bwd=r)
+    layer = MoELayer(cfg, init_seed=seed)
+    dt = layer.act_dtype
+    g = torch.Generator().manual_seed(seed + 100)
+    x = (torch.rand(T, M, generator=g) * 2 - 1).to("cuda", dt)
+    dy = (torch.rand(T, M, generator=g) * 2 - 1).to("cuda", dt)
+    y = layer.forward(x)
+    dx = layer.backward(dy)
+    torch.cuda.synchronize()
+
+    xn = x.double().cpu().numpy()
+    wg = layer.w_gate.cpu().numpy()
+    wn = layer.w_noise.cpu().numpy()
+    pj = layer.proj.cpu().numpy() if layer.proj is not None else None
+    W1 = layer.w1.double().cpu().numpy()
+    W2 = layer.w2.double().cpu().numpy()
+    kk = layer.capacity if gate == "expert_choice" else k
+    orc = pyoracle.Oracle("port")
+    yr, cache = layer_oracle.forward(xn, gate, kk, 11, layer.capacity, wg, wn, pj, W1, W2, ffn, orc)
+    ref = layer_oracle.backward(cache, dy.double().cpu().numpy(), gate, kk, layer.capacity, wg, wn,
+                                pj, W1, W2, ffn)
+    # routing inside the layer is bit-exact
+    n = cache.picks.token.size
+    np.testing.assert_array_equal(layer.buffer("pick_token", torch.int32)[:n].cpu().numpy(),
+                                  cache.picks.token)
+    np.testing.assert_array_equal(layer.buffer("pick_expert", torch.int32)[:n].cpu().numpy(),
+                                  cache.picks.expert)
+    np.testing.assert_array_equal(layer.buffer("slot_of_pick", torch.int32)[:n].cpu().numpy(),
+                                  cache.disp.slot_of_pick)
+    np.testing.assert_array_equal(layer.buffer("fill", torch.int64).cpu().numpy(), cache.disp.fill)
+    return layer, y, dx, yr, ref
+
+
+TOL = {"f32": 1e-4, "bf16": 3e-2}
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+@pytest.mark.parametrize("gate", ["noisy_topk", "sigmoid_topk", "cosine_topk", "expert_choice"])
+@pytest.mark.parametrize("ffn", ["simple", "gated3"])
+def test_layer_fwd_bwd_vs_oracle(precision, gate, ffn):
+    layer, y, dx, yr, ref = _run(gate, ffn, precision)
+    tol = TOL[precision]
+    assert _rel(y, yr) < tol
+    assert _rel(dx, ref["dx"]) < tol
+    assert _rel(layer.g_w1, ref["g_w1"]) < tol
+    assert _rel(layer.g_w2, ref["g_w2"]) < tol
+    if np.max(np.abs(ref["g_gate"])) > 0:
+        assert _rel(layer.g_gate, ref["g_gate"]) < tol
+    if gate == "noisy_topk" and np.max(np.abs(ref["g_noise"])) > 0:
+        assert _rel(layer.g_noise, ref["g_noise"]) < tol
+    if gate == "cosine_topk":
+        assert _rel(layer.g_proj, ref["g_proj"]) < tol
+
+
+@pytest.mark.parametrize("r", [2, 3])
+def test_pipeline_degree_does_not_change_results(r):
+    """Chunked execution (r > 1) on one GPU == r = 1 (forward exactly; wgrad
+    within fp32 re-association)."""
+    l1, y1, dx1, _, _ = _run("noisy_topk", "simple", "bf16", T=1024, cap=512, r=1)
+    lr, yr, dxr, _, _ = _run("noisy_topk", "simple", "bf16", T=1024, cap=512, r=r)
+    assert torch.equal(y1, yr)
+    assert torch.equal(dx1, dxr)
+    assert _rel(lr.g_w1, l1.g_w1.double().cpu().numpy()) < 1e-5
+
+
+def test_config1_shape_check_mode():
+    """BASELINE config 1 (T=4096, M=512, H=2048, E=8, k=2, f=1.0, fp32)."""
+    layer, y, dx, yr, ref = _run("noisy_topk", "simple", "f32", T=4096, M=512, H=2048, E=8, k=2)
+    assert _rel(y, yr) < 1e-4
+    assert _rel(dx, ref["dx"]) < 1e-4
+    assert _rel(layer.g_w1, ref["g_w1"]) < 1e-4
+    assert _rel(layer.g_w2, ref["g_w2"]) < 1e-4
+    assert _rel(layer.g_gate, ref["g_gate"]) < 1e-4
