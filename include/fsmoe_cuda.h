@@ -48,6 +48,8 @@ int fsmoe_abi_version(void);
  * the calling thread. */
 int fsmoe_copy_device(void* dst, const void* src, size_t bytes, void* stream);
 int fsmoe_set_device(int device);
+/* Number of kernels launched by this library since load (bench evidence). */
+long long fsmoe_launch_count(void);
 
 /* ---------------------------------------------------------------- routing --
  * Replaces fsmoe::run_gate (workload.hpp:110-111, workload.cpp:143-235).

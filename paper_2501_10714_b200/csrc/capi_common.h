@@ -15,6 +15,9 @@ int cuda_status(cudaError_t e, const char* where);  // 0 or FSMOE_CUDA_ERROR
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Process-wide count of kernels this library has launched (fsmoe_launch_count).
+void count_launch();
+
 }  // namespace fsmoe
 
 #define FSMOE_CUDA_TRY(expr, where)                         \

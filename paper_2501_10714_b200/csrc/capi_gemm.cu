@@ -1,4 +1,5 @@
 // capi_gemm.cu — extern "C" error plumbing + expert-FFN GEMM entry points.
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -8,6 +9,9 @@
 namespace fsmoe {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
@@ -88,6 +92,8 @@ const char* fsmoe_last_error(void) { return fsmoe::g_last_error.c_str(); }
 
 int fsmoe_abi_version(void) { return 1; }
 
+long long fsmoe_launch_count(void) { return fsmoe::g_launches.load(); }
+
 int fsmoe_copy_device(void* dst, const void* src, size_t bytes, void* stream) {
   FSMOE_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, fsmoe::as_stream(stream)),
                  "fsmoe_copy_device");
@@ -144,7 +150,7 @@ int fsmoe_activation_f32(int op, int nblk, int rows_total, int row0, int rows, i
   long long n = static_cast<long long>(nblk) * rows * units;
   int grid = static_cast<int>((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
   act_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(op, nblk, rows_total, row0, rows, units, in,
-                                                      z, out);
+                                                      z, out); ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_activation_f32");
 }
 

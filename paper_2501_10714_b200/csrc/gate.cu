@@ -31,39 +31,64 @@ namespace {
 
 using namespace fsmoe_dev;
 
-constexpr int RD_THREADS = 64;  // tokens per block
-constexpr int RD_CG = 16;       // output columns per pass
-constexpr int RD_JC = 128;      // reduction chunk staged in smem
+constexpr int RD_THREADS = 128;  // tokens per block (one per thread)
+constexpr int RD_CG = 8;         // output columns per thread
 
-// out[t*ost + c*osc] = sum_j x[t][j] * W[j*wsj + c*wsc]   (c < NC)
+struct RowdotJob {
+  const double* W;  // W(j, c) = W[j*wsj + c*wsc]
+  long long wsj, wsc;
+  int NC;
+  double* out;      // out[t*ost + c*osc]
+  long long ost, osc;
+};
+
+// Token chunk staging type: bf16/fp32 values are exact in fp32, fp64 stays fp64.
+template <int DT> struct Stage { using T = float; static constexpr int JC = 64; };
+template <> struct Stage<0> { using T = double; static constexpr int JC = 32; };
+
+// out[t][c] = sum_j x[t][j] * W(j, c), sequential j, separately rounded
+// mul/add (matvec_row, workload.cpp:103-108). One thread = one token x 8
+// columns; blockIdx.y walks the column groups of job a, then of job b, so the
+// noisy gate's two projections (x W_g, x W_noise) are one launch. The token
+// chunk is staged transposed in smem (conflict-free reads), the weight chunk
+// as broadcast rows.
 template <int DT>
 __global__ void __launch_bounds__(RD_THREADS)
-    rowdot_kernel(const void* __restrict__ x, int T, int M, const double* __restrict__ W,
-                  long long wsj, long long wsc, int NC, double* __restrict__ out, long long ost,
-                  long long osc) {
-  __shared__ __align__(16) double ws[RD_JC][RD_CG];
-  const int t = blockIdx.x * RD_THREADS + threadIdx.x;
-  const int c0 = blockIdx.y * RD_CG;
+    rowdot_kernel(const void* __restrict__ x, int T, int M, RowdotJob ja, RowdotJob jb,
+                  int groups_a) {
+  using ST = typename Stage<DT>::T;
+  constexpr int JC = Stage<DT>::JC;
+  __shared__ __align__(16) ST xs[JC][RD_THREADS];
+  __shared__ __align__(16) double ws[JC][RD_CG];
+  const bool second = static_cast<int>(blockIdx.y) >= groups_a;
+  const RowdotJob& J = second ? jb : ja;
+  const int c0 = (second ? blockIdx.y - groups_a : blockIdx.y) * RD_CG;
+  const int t0 = blockIdx.x * RD_THREADS;
+  const int t = t0 + threadIdx.x;
   double acc[RD_CG];
 #pragma unroll
   for (int c = 0; c < RD_CG; ++c) acc[c] = 0.0;
-  const long long xrow = static_cast<long long>(t) * M;
-  for (int j0 = 0; j0 < M; j0 += RD_JC) {
+  for (int j0 = 0; j0 < M; j0 += JC) {
+    const int jn = (M - j0) < JC ? (M - j0) : JC;
     __syncthreads();
-    for (int i = threadIdx.x; i < RD_JC * RD_CG; i += RD_THREADS) {
+    for (int i = threadIdx.x; i < JC * RD_CG; i += RD_THREADS) {
       int jj = i / RD_CG, cc = i % RD_CG;
-      int j = j0 + jj, c = c0 + cc;
-      ws[jj][cc] = (j < M && c < NC) ? W[j * wsj + c * wsc] : 0.0;
+      int c = c0 + cc;
+      ws[jj][cc] = (jj < jn && c < J.NC) ? J.W[(j0 + jj) * J.wsj + c * J.wsc] : 0.0;
+    }
+    if (t < T) {
+      const long long base = static_cast<long long>(t) * M + j0;
+      for (int jj = 0; jj < jn; ++jj) xs[jj][threadIdx.x] = static_cast<ST>(load_as_double<DT>(x, base + jj));
     }
     __syncthreads();
     if (t < T) {
-      const int jn = (M - j0) < RD_JC ? (M - j0) : RD_JC;
+#pragma unroll 4
       for (int jj = 0; jj < jn; ++jj) {
-        const double xv = load_as_double<DT>(x, xrow + j0 + jj);
+        const double xv = static_cast<double>(xs[jj][threadIdx.x]);
         const double2* w2 = reinterpret_cast<const double2*>(ws[jj]);
 #pragma unroll
         for (int c = 0; c < RD_CG / 2; ++c) {
-          double2 w = w2[c];
+          const double2 w = w2[c];
           acc[2 * c] = mul_add_rn(acc[2 * c], xv, w.x);
           acc[2 * c + 1] = mul_add_rn(acc[2 * c + 1], xv, w.y);
         }
@@ -73,7 +98,7 @@ __global__ void __launch_bounds__(RD_THREADS)
   if (t < T) {
 #pragma unroll
     for (int c = 0; c < RD_CG; ++c)
-      if (c0 + c < NC) out[t * ost + (c0 + c) * osc] = acc[c];
+      if (c0 + c < J.NC) J.out[t * J.ost + (c0 + c) * J.osc] = acc[c];
   }
 }
 
@@ -97,9 +122,10 @@ __device__ __forceinline__ uint64_t mt_seed_step(uint64_t prev, uint64_t i) {
 
 // First n outputs of std::mt19937_64(seed) (libstdc++ twists all 312 words on
 // the first draw; output i < 156 only needs seed words i, i+1, i+156).
+template <int MAXN>
 __device__ void mt64_outputs(uint64_t seed, int n, uint64_t* outv) {
-  if (n <= 156) {
-    uint64_t lo[157];
+  if constexpr (MAXN <= 156) {
+    uint64_t lo[MAXN + 1];
     uint64_t w = seed;
     lo[0] = w;
     for (int i = 1; i < 156 + n; ++i) {
@@ -112,21 +138,21 @@ __device__ void mt64_outputs(uint64_t seed, int n, uint64_t* outv) {
         outv[o] = mt_temper(z);
       }
     }
-    return;
-  }
-  uint64_t mt[312];
-  mt[0] = seed;
-  for (int i = 1; i < 312; ++i) mt[i] = mt_seed_step(mt[i - 1], static_cast<uint64_t>(i));
-  int idx = 312;
-  for (int o = 0; o < n; ++o) {
-    if (idx >= 312) {
-      for (int i = 0; i < 312; ++i) {
-        uint64_t y = (mt[i] & MT_UM) | (mt[(i + 1) % 312] & MT_LM);
-        mt[i] = mt[(i + 156) % 312] ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL);
+  } else {
+    uint64_t mt[312];
+    mt[0] = seed;
+    for (int i = 1; i < 312; ++i) mt[i] = mt_seed_step(mt[i - 1], static_cast<uint64_t>(i));
+    int idx = 312;
+    for (int o = 0; o < n; ++o) {
+      if (idx >= 312) {
+        for (int i = 0; i < 312; ++i) {
+          uint64_t y = (mt[i] & MT_UM) | (mt[(i + 1) % 312] & MT_LM);
+          mt[i] = mt[(i + 156) % 312] ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL);
+        }
+        idx = 0;
       }
-      idx = 0;
+      outv[o] = mt_temper(mt[idx++]);
     }
-    outv[o] = mt_temper(mt[idx++]);
   }
 }
 
@@ -140,9 +166,7 @@ __device__ __forceinline__ double box_muller(uint64_t a, uint64_t b) {
 
 // ------------------------------------------------------- token selection --
 
-constexpr int MAX_E = 256;
-
-template <int KIND>
+template <int KIND, int MAX_E>
 __global__ void __launch_bounds__(128)
     token_select_kernel(int T, int E, int k, uint64_t seed, const double* __restrict__ raw,
                         const double* __restrict__ spread, int P,
@@ -155,7 +179,7 @@ __global__ void __launch_bounds__(128)
   double s[MAX_E];
   if (KIND == 0) {  // noisy_topk
     uint64_t draws[2 * MAX_E];
-    mt64_outputs(seed + static_cast<uint64_t>(t), 2 * E, draws);
+    mt64_outputs<2 * MAX_E>(seed + static_cast<uint64_t>(t), 2 * E, draws);
     for (int e = 0; e < E; ++e) {
       double n = box_muller(draws[2 * e], draws[2 * e + 1]);
       double sp = log1p(exp(spread[static_cast<long long>(t) * E + e]));
@@ -188,8 +212,8 @@ __global__ void __launch_bounds__(128)
 
   // top-k: repeatedly take the max with ties to the lowest index, then
   // report the kept set in ascending index order.
-  uint32_t sel[MAX_E / 32];
-  for (int i = 0; i < MAX_E / 32; ++i) sel[i] = 0;
+  uint32_t sel[(MAX_E + 31) / 32];
+  for (int i = 0; i < (MAX_E + 31) / 32; ++i) sel[i] = 0;
   for (int j = 0; j < k; ++j) {
     int best = -1;
     for (int e = 0; e < E; ++e) {
@@ -221,6 +245,24 @@ __global__ void __launch_bounds__(128)
     pick_expert[base + j] = keep[j];
     pick_weight[base + j] = __ddiv_rn(exp(__dsub_rn(s[keep[j]], mx)), z);
   }
+}
+
+template <int KIND>
+void launch_select(cudaStream_t st, int T, int E, int k, uint64_t seed, const double* raw,
+                   const double* spread, int P, const double* w_score, const double* enorm,
+                   int* pt, int* pe, double* pw, double* scores_out, double* noise_out,
+                   int* status) {
+  const int blocks = (T + 127) / 128;
+  if (E <= 16)
+    token_select_kernel<KIND, 16><<<blocks, 128, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
+                                                          enorm, pt, pe, pw, scores_out, noise_out, status);
+  else if (E <= 64)
+    token_select_kernel<KIND, 64><<<blocks, 128, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
+                                                          enorm, pt, pe, pw, scores_out, noise_out, status);
+  else
+    token_select_kernel<KIND, 256><<<blocks, 128, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
+                                                           enorm, pt, pe, pw, scores_out, noise_out, status);
+  ::fsmoe::count_launch();
 }
 
 // enorm[e] = sum_p W[p][e]^2 (same order as the reference's per-token loop).
@@ -357,7 +399,7 @@ __global__ void __launch_bounds__(EC_THREADS)
 // ---------------------------------------------------------------- host ----
 
 void cosine_enorm(int P, int E, const double* w, double* en, cudaStream_t st) {
-  expert_norm_kernel<<<(E + 127) / 128, 128, 0, st>>>(P, E, w, en);
+  expert_norm_kernel<<<(E + 127) / 128, 128, 0, st>>>(P, E, w, en); ::fsmoe::count_launch();
 }
 
 int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
@@ -372,40 +414,35 @@ int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
     w += (bytes + 255) & ~size_t(255);
     return reinterpret_cast<double*>(p);
   };
+  auto rowdot2 = [&](RowdotJob a, RowdotJob b) {
+    const int ga = (a.NC + RD_CG - 1) / RD_CG, gb = b.W ? (b.NC + RD_CG - 1) / RD_CG : 0;
+    dim3 grid((T + RD_THREADS - 1) / RD_THREADS, ga + gb);
+    switch (d.x_dtype) {
+      case FSMOE_F64: rowdot_kernel<0><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
+      case FSMOE_F32: rowdot_kernel<1><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
+      default: rowdot_kernel<2><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
+    }
+    ::fsmoe::count_launch();
+  };
   auto rowdot = [&](const double* W, long long wsj, long long wsc, int NC, double* out,
                     long long ost, long long osc) {
-    dim3 grid((T + RD_THREADS - 1) / RD_THREADS, (NC + RD_CG - 1) / RD_CG);
-    switch (d.x_dtype) {
-      case FSMOE_F64:
-        rowdot_kernel<0><<<grid, RD_THREADS, 0, st>>>(x, T, M, W, wsj, wsc, NC, out, ost, osc);
-        break;
-      case FSMOE_F32:
-        rowdot_kernel<1><<<grid, RD_THREADS, 0, st>>>(x, T, M, W, wsj, wsc, NC, out, ost, osc);
-        break;
-      default:
-        rowdot_kernel<2><<<grid, RD_THREADS, 0, st>>>(x, T, M, W, wsj, wsc, NC, out, ost, osc);
-        break;
-    }
+    rowdot2(RowdotJob{W, wsj, wsc, NC, out, ost, osc}, RowdotJob{nullptr, 0, 0, 0, nullptr, 0, 0});
   };
   (void)ws_bytes;
-  const int sel_blocks = (T + 127) / 128;
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
       double* raw = take(sizeof(double) * T * E);
       double* spread = spread_out ? spread_out : take(sizeof(double) * T * E);
-      rowdot(w_score, E, 1, E, raw, E, 1);
-      rowdot(w_noise, E, 1, E, spread, E, 1);
-      token_select_kernel<0><<<sel_blocks, 128, 0, st>>>(
-          T, E, k, d.seed, raw, spread, 0, nullptr, nullptr, pick_token, pick_expert,
-          pick_weight, scores_out, noise_out, d_status);
+      rowdot2(RowdotJob{w_score, E, 1, E, raw, E, 1}, RowdotJob{w_noise, E, 1, E, spread, E, 1});
+      launch_select<0>(st, T, E, k, d.seed, raw, spread, 0, nullptr, nullptr, pick_token,
+                       pick_expert, pick_weight, scores_out, noise_out, d_status);
       break;
     }
     case FSMOE_GATE_SIGMOID_TOPK: {
       double* raw = scores_out ? scores_out : take(sizeof(double) * T * E);
       rowdot(w_score, E, 1, E, raw, E, 1);
-      token_select_kernel<1><<<sel_blocks, 128, 0, st>>>(
-          T, E, k, d.seed, raw, nullptr, 0, nullptr, nullptr, pick_token, pick_expert,
-          pick_weight, nullptr, nullptr, d_status);
+      launch_select<1>(st, T, E, k, d.seed, raw, nullptr, 0, nullptr, nullptr, pick_token,
+                       pick_expert, pick_weight, nullptr, nullptr, d_status);
       break;
     }
     case FSMOE_GATE_COSINE_TOPK: {
@@ -414,17 +451,16 @@ int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
       double* en = take(sizeof(double) * E);
       // proj[p] = sum_j P[p][j] * x[j]  -> W(j, p) = P[p*M + j]
       rowdot(proj, 1, M, P, q, P, 1);
-      expert_norm_kernel<<<(E + 127) / 128, 128, 0, st>>>(P, E, w_score, en);
-      token_select_kernel<2><<<sel_blocks, 128, 0, st>>>(
-          T, E, k, d.seed, q, nullptr, P, w_score, en, pick_token, pick_expert, pick_weight,
-          scores_out, nullptr, d_status);
+      expert_norm_kernel<<<(E + 127) / 128, 128, 0, st>>>(P, E, w_score, en); ::fsmoe::count_launch();
+      launch_select<2>(st, T, E, k, d.seed, q, nullptr, P, w_score, en, pick_token, pick_expert,
+                       pick_weight, scores_out, nullptr, d_status);
       break;
     }
     case FSMOE_GATE_EXPERT_CHOICE: {
       double* sc = scores_out ? scores_out : take(sizeof(double) * T * E);  // E x T
       rowdot(w_score, E, 1, E, sc, 1, T);
       ec_select_kernel<<<E, EC_THREADS, 0, st>>>(T, E, k, sc, pick_token, pick_expert,
-                                                 pick_weight);
+                                                 pick_weight); ::fsmoe::count_launch();
       break;
     }
     default:

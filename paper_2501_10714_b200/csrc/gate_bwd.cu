@@ -223,22 +223,22 @@ void xtg(int xdt, int T, int M, int NC, const void* X, const double* G, long lon
   const int nchunks = (T + XT_TCH - 1) / XT_TCH;
   dim3 grid((M + XT_J - 1) / XT_J, (NC + XT_C - 1) / XT_C, nchunks);
   switch (xdt) {
-    case FSMOE_F64: xtg_partial_kernel<0><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
-    case FSMOE_F32: xtg_partial_kernel<1><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
-    default: xtg_partial_kernel<2><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+    case FSMOE_F64: xtg_partial_kernel<0><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
+    case FSMOE_F32: xtg_partial_kernel<1><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
+    default: xtg_partial_kernel<2><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
   }
   long long n = static_cast<long long>(M) * NC;
   xtg_reduce_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(nchunks, M, NC, part, out,
-                                                                       osj, osc, accumulate);
+                                                                       osj, osc, accumulate); ::fsmoe::count_launch();
 }
 
 void dx_acc(int xdt, int T, int M, int NC, const double* G, long long gst, long long gsc,
             const double* W, long long wsj, long long wsc, void* dx, cudaStream_t st) {
   dim3 grid((M + 255) / 256, (T + 31) / 32);
   switch (xdt) {
-    case FSMOE_F64: dx_acc_kernel<double><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<double*>(dx)); break;
-    case FSMOE_F32: dx_acc_kernel<float><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<float*>(dx)); break;
-    default: dx_acc_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<__nv_bfloat16*>(dx)); break;
+    case FSMOE_F64: dx_acc_kernel<double><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<double*>(dx)); ::fsmoe::count_launch(); break;
+    case FSMOE_F32: dx_acc_kernel<float><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<float*>(dx)); ::fsmoe::count_launch(); break;
+    default: dx_acc_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<__nv_bfloat16*>(dx)); ::fsmoe::count_launch(); break;
   }
 }
 
@@ -259,6 +259,12 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
                     const double* spread, const double* proj_out, void* dx, double* dWs,
                     double* dWn, double* dP, void* ws, cudaStream_t st) {
   const int T = d.tokens, M = d.model_dim, E = d.score_cols, k = d.top_k;
+  // A softmax over a single survivor is the constant 1 (workload.cpp:123-133
+  // with one kept index): dS = w*(dw - w*dw) = 0 exactly, so every gate
+  // gradient contribution vanishes (Switch-style top-1).
+  const bool softmax_gate = d.kind == FSMOE_GATE_NOISY_TOPK || d.kind == FSMOE_GATE_COSINE_TOPK ||
+                            d.kind == FSMOE_GATE_EXPERT_CHOICE;
+  if (softmax_gate && k == 1) return FSMOE_OK;
   Ws w{static_cast<char*>(ws)};
   double* dS = w.take(static_cast<size_t>(T) * E);
   const int nch = (T + XT_TCH - 1) / XT_TCH;
@@ -267,10 +273,10 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
   double* part = w.take(static_cast<size_t>(nch) * (M > P ? M : P) * (nc > 0 ? nc : 1));
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
-      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS);
+      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dZ = w.take(static_cast<size_t>(T) * E);
       long long n = static_cast<long long>(T) * E;
-      noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ);
+      noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ); ::fsmoe::count_launch();
       xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
       xtg(d.x_dtype, T, M, E, x, dZ, E, 1, dWn, E, 1, 1, part, st);
       dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
@@ -278,19 +284,19 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       break;
     }
     case FSMOE_GATE_SIGMOID_TOPK: {
-      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(1, T, E, k, pexp, pw, dw, dS);
+      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(1, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
       dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
       break;
     }
     case FSMOE_GATE_EXPERT_CHOICE: {
-      dscore_ec_kernel<<<E, 256, 0, st>>>(T, E, k, ptok, pw, dw, dS);  // E x T
+      dscore_ec_kernel<<<E, 256, 0, st>>>(T, E, k, ptok, pw, dw, dS); ::fsmoe::count_launch();  // E x T
       xtg(d.x_dtype, T, M, E, x, dS, 1, T, dWs, E, 1, 1, part, st);
       dx_acc(d.x_dtype, T, M, E, dS, 1, T, w_score, E, 1, dx, st);
       break;
     }
     case FSMOE_GATE_COSINE_TOPK: {
-      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS);
+      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dq = w.take(static_cast<size_t>(T) * P);
       double* qn = w.take(static_cast<size_t>(T) * P);
       double* en = w.take(E);
@@ -299,10 +305,10 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       // enorm recomputed (cheap) with the forward's arithmetic
       cosine_enorm(P, E, w_score, en, st);
       cosine_dq_kernel<<<(T + 127) / 128, 128, 0, st>>>(T, E, P, proj_out, w_score, en, scores, dS,
-                                                       dq, qn);
-      cosine_b_kernel<<<E, 256, 0, st>>>(T, E, scores, dS, bb);
+                                                       dq, qn); ::fsmoe::count_launch();
+      cosine_b_kernel<<<E, 256, 0, st>>>(T, E, scores, dS, bb); ::fsmoe::count_launch();
       xtg(FSMOE_F64, T, P, E, qn, dS, E, 1, A, E, 1, 0, part, st);
-      cosine_dw_kernel<<<(P * E + 255) / 256, 256, 0, st>>>(P, E, A, w_score, en, bb, dWs);
+      cosine_dw_kernel<<<(P * E + 255) / 256, 256, 0, st>>>(P, E, A, w_score, en, bb, dWs); ::fsmoe::count_launch();
       // dProj[p][j] += sum_t dq[t][p] x[t][j]
       xtg(d.x_dtype, T, M, P, x, dq, P, 1, dP, 1, M, 1, part, st);
       // dx += dq . Proj  (W(j,p) = Proj[p*M + j])

@@ -72,4 +72,6 @@ int gemm_sm100_launch(const GemmProblem& p, cudaStream_t stream);
 // fp32 operands/outputs, SIMT FFMA; same problem semantics (check mode).
 int gemm_simt_launch(const GemmProblem& p, cudaStream_t stream);
 
+void count_launch();  // capi_gemm.cu
+
 }  // namespace fsmoe

@@ -139,7 +139,7 @@ int gemm_simt_launch(const GemmProblem& pr, cudaStream_t stream) {
     if (pr.nblk % p.n_w) return cudaErrorInvalidValue;
     grid = dim3((pr.No + TN - 1) / TN, (pr.Mo + TM - 1) / TM, p.n_w);
   }
-  simt_gemm_kernel<<<grid, 256, 0, stream>>>(p);
+  simt_gemm_kernel<<<grid, 256, 0, stream>>>(p); ::fsmoe::count_launch();
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -11,7 +11,8 @@
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      MMA issuer (one elected lane)
 //   warp 2      TMEM allocator
-//   warps 4..7  epilogue: TMEM -> registers -> activation -> global
+//   warps 4..11 epilogue: TMEM -> registers -> activation -> global; warp w
+//               reads TMEM lane quarter w%4 and column half (w-4)/4
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -33,7 +34,8 @@ constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;
+constexpr int EPI_THREADS = 256;  // 8 epilogue warps
 constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], EPI_THREADS);
     }
     fence_barrier_init();
   }
@@ -254,6 +256,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;
+    const int half = (warp - 4) >> 2;  // which 128 accumulator columns
     const int lane = threadIdx.x & 31;
     int acc = 0;
     uint32_t aph = 0;
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
         __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) +
                            orow * p.ldd2;
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 2 * half; c < 2 * half + 2; ++c) {
           float g[32];
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       } else {
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 4 * half; c < 4 * half + 4; ++c) {
           const int col = ti.nt * BN + c * 32;
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
@@ -503,7 +506,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     attr_set = true;
   }
   int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
-  grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
+  grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p); ::fsmoe::count_launch();
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -29,7 +29,7 @@ namespace {
 using namespace fsmoe_dev;
 
 constexpr int AS_THREADS = 1024;
-constexpr int AS_TILE = 4 * AS_THREADS;  // picks per tile
+constexpr int AS_TILE = AS_THREADS;  // picks per tile (one round per block)
 constexpr int AS_MAX_E = 256;
 
 // cnt[tile][e] = picks of expert e inside the tile; flags bad picks.
@@ -251,11 +251,84 @@ __device__ __forceinline__ double madd(double acc, double w, double b) {
 }
 __device__ __forceinline__ float madd(float acc, float w, float b) { return fmaf(w, b, acc); }
 
-// 8 elements per lane per step (16 B of bf16 / 32 B fp32 / 64 B fp64).
+// 8 consecutive elements per lane per vector (16 B bf16 / 32 B fp32 / 64 B fp64),
+// 4 vectors in flight per lane: one warp covers 1024 columns per pass.
 constexpr int CV = 8;
+constexpr int NV = 4;
+
+template <typename T>
+struct Vec8;
+template <>
+struct Vec8<__nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float* o) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      o[2 * i] = f.x;
+      o[2 * i + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float* v) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+template <>
+struct Vec8<float> {
+  static __device__ __forceinline__ void ld(const float* p, float* o) {
+    float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float* v) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+template <>
+struct Vec8<double> {
+  static __device__ __forceinline__ void ld(const double* p, double* o) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double2 d = reinterpret_cast<const double2*>(p)[i];
+      o[2 * i] = d.x;
+      o[2 * i + 1] = d.y;
+    }
+  }
+  static __device__ __forceinline__ void st(double* p, const double* v) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) reinterpret_cast<double2*>(p)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+  }
+};
+
+// Load / store 8 elements at column j of a row; VEC: full aligned vector,
+// otherwise bounds-checked scalars.
+template <bool VEC, typename T, typename A>
+__device__ __forceinline__ void ld8(const T* row, int j, int M, A* o) {
+  if (VEC) {
+    Vec8<T>::ld(row + j, o);
+  } else {
+#pragma unroll
+    for (int v = 0; v < CV; ++v) o[v] = j + v < M ? Acc<T>::ld(row, j + v) : A(0);
+  }
+}
+template <bool VEC, typename T, typename A>
+__device__ __forceinline__ void st8(T* row, int j, int M, const A* x) {
+  if (VEC) {
+    Vec8<T>::st(row + j, x);
+  } else {
+#pragma unroll
+    for (int v = 0; v < CV; ++v)
+      if (j + v < M) Acc<T>::st(row, j + v, x[v]);
+  }
+}
 
 // y[t] = sum_{kept picks of t, pick order} w * buf[row(slot)]; one warp per token.
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256)
     combine_kernel(int ntok, int M, int E, long long C, int chunks, const int* __restrict__ tptr,
                    const int* __restrict__ tpick, const int* __restrict__ slot_of_pick,
@@ -266,28 +339,39 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31;
   const int a = tptr[t], b = tptr[t + 1];
   T* yr = y + static_cast<long long>(t) * M;
-  for (int j0 = lane * CV; j0 < M; j0 += 32 * CV) {
-    A acc[CV];
+  for (int jb = 0; jb < M; jb += 32 * CV * NV) {
+    A acc[NV][CV];
 #pragma unroll
-    for (int v = 0; v < CV; ++v) acc[v] = A(0);
+    for (int u = 0; u < NV; ++u)
+#pragma unroll
+      for (int v = 0; v < CV; ++v) acc[u][v] = A(0);
     for (int q = a; q < b; ++q) {
       const int p = tpick[q];
       const int s = slot_of_pick[p];
       if (s < 0) continue;
       const A w = static_cast<A>(pw[p]);
       const T* br = buf + slot_row(s, E, C, chunks) * M;
+      A val[NV][CV];
 #pragma unroll
-      for (int v = 0; v < CV; ++v)
-        if (j0 + v < M) acc[v] = madd(acc[v], w, Acc<T>::ld(br, j0 + v));
+      for (int u = 0; u < NV; ++u) {
+        const int j = jb + (u * 32 + lane) * CV;
+        if (j < M) ld8<VEC>(br, j, M, val[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < NV; ++u)
+#pragma unroll
+        for (int v = 0; v < CV; ++v) acc[u][v] = madd(acc[u][v], w, val[u][v]);
     }
 #pragma unroll
-    for (int v = 0; v < CV; ++v)
-      if (j0 + v < M) Acc<T>::st(yr, j0 + v, acc[v]);
+    for (int u = 0; u < NV; ++u) {
+      const int j = jb + (u * 32 + lane) * CV;
+      if (j < M) st8<VEC>(yr, j, M, acc[u]);
+    }
   }
 }
 
 // dx[t] (+)= sum_{kept picks of t} dbuf[row(slot)]
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256)
     dispatch_bwd_kernel(int ntok, int M, int E, long long C, int chunks,
                         const int* __restrict__ tptr, const int* __restrict__ tpick,
@@ -299,26 +383,43 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31;
   const int a = tptr[t], b = tptr[t + 1];
   T* xr = dx + static_cast<long long>(t) * M;
-  for (int j0 = lane * CV; j0 < M; j0 += 32 * CV) {
-    A acc[CV];
+  for (int jb = 0; jb < M; jb += 32 * CV * NV) {
+    A acc[NV][CV];
 #pragma unroll
-    for (int v = 0; v < CV; ++v) acc[v] = (accumulate && j0 + v < M) ? Acc<T>::ld(xr, j0 + v) : A(0);
+    for (int u = 0; u < NV; ++u) {
+      const int j = jb + (u * 32 + lane) * CV;
+      if (accumulate && j < M) {
+        ld8<VEC>(xr, j, M, acc[u]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < CV; ++v) acc[u][v] = A(0);
+      }
+    }
     for (int q = a; q < b; ++q) {
       const int s = slot_of_pick[tpick[q]];
       if (s < 0) continue;
       const T* br = dbuf + slot_row(s, E, C, chunks) * M;
+      A val[NV][CV];
 #pragma unroll
-      for (int v = 0; v < CV; ++v)
-        if (j0 + v < M) acc[v] = acc[v] + Acc<T>::ld(br, j0 + v);
+      for (int u = 0; u < NV; ++u) {
+        const int j = jb + (u * 32 + lane) * CV;
+        if (j < M) ld8<VEC>(br, j, M, val[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < NV; ++u)
+#pragma unroll
+        for (int v = 0; v < CV; ++v) acc[u][v] = acc[u][v] + val[u][v];
     }
 #pragma unroll
-    for (int v = 0; v < CV; ++v)
-      if (j0 + v < M) Acc<T>::st(xr, j0 + v, acc[v]);
+    for (int u = 0; u < NV; ++u) {
+      const int j = jb + (u * 32 + lane) * CV;
+      if (j < M) st8<VEC>(xr, j, M, acc[u]);
+    }
   }
 }
 
 // dbuf[row(s)] = w_p * dy[t_p] (0 for padding); dw[p] = <dy[t_p], buf[row(s)]>.
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256)
     combine_bwd_kernel(long long n_slots, int M, int E, long long C, int chunks,
                        const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
@@ -332,20 +433,37 @@ __global__ void __launch_bounds__(256)
   const long long row = slot_row(s, E, C, chunks);
   T* dr = dbuf + row * M;
   if (p < 0) {
-    for (int j = lane; j < M; j += 32) Acc<T>::st(dr, j, A(0));
+    A z[CV];
+#pragma unroll
+    for (int v = 0; v < CV; ++v) z[v] = A(0);
+    for (int j = lane * CV; j < M; j += 32 * CV) st8<VEC>(dr, j, M, z);
     return;
   }
   const A w = static_cast<A>(pw[p]);
   const T* g = dy + static_cast<long long>(ptok[p]) * M;
   const T* o = buf + row * M;
   A dot = A(0);
-  for (int j0 = lane * CV; j0 < M; j0 += 32 * CV) {
+  for (int jb = 0; jb < M; jb += 32 * CV * NV) {
+    A gv[NV][CV], ov[NV][CV];
 #pragma unroll
-    for (int v = 0; v < CV; ++v) {
-      if (j0 + v >= M) break;
-      A gv = Acc<T>::ld(g, j0 + v);
-      Acc<T>::st(dr, j0 + v, static_cast<A>(w * gv));
-      dot = madd(dot, gv, Acc<T>::ld(o, j0 + v));
+    for (int u = 0; u < NV; ++u) {
+      const int j = jb + (u * 32 + lane) * CV;
+      if (j < M) {
+        ld8<VEC>(g, j, M, gv[u]);
+        ld8<VEC>(o, j, M, ov[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int j = jb + (u * 32 + lane) * CV;
+      if (j >= M) continue;
+      A out[CV];
+#pragma unroll
+      for (int v = 0; v < CV; ++v) {
+        out[v] = static_cast<A>(w * gv[u][v]);
+        dot = madd(dot, gv[u][v], ov[u][v]);
+      }
+      st8<VEC>(dr, j, M, out);
     }
   }
   for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
@@ -386,9 +504,9 @@ int assign_launch(long long P, const int* ptok, const int* pexp, int T, int E, l
   }
   int ntiles = static_cast<int>((P + AS_TILE - 1) / AS_TILE);
   int* cnt = static_cast<int*>(ws);
-  assign_count_kernel<<<ntiles, AS_THREADS, 0, st>>>(P, ptok, pexp, T, E, cnt, status);
+  assign_count_kernel<<<ntiles, AS_THREADS, 0, st>>>(P, ptok, pexp, T, E, cnt, status); ::fsmoe::count_launch();
   assign_rank_kernel<<<ntiles, AS_THREADS, 0, st>>>(P, pexp, E, C, cnt, ntiles, slot_of_pick,
-                                                    pick_of_slot, fill, dropped);
+                                                    pick_of_slot, fill, dropped); ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_assign");
 }
 
@@ -400,17 +518,17 @@ int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, in
                        void* ws, cudaStream_t st) {
   if (k > 0) {
     long long n = (static_cast<long long>(T) * k > T + 1) ? static_cast<long long>(T) * k : T + 1;
-    tok_token_major_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(T, k, tptr, tpick);
+    tok_token_major_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(T, k, tptr, tpick); ::fsmoe::count_launch();
     return cuda_status(cudaGetLastError(), "fsmoe_token_index");
   }
   int* cnt = static_cast<int*>(ws);
   int* cursor = cnt + (T + 1);
   FSMOE_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (T + 1) * 2, st), "token_index memset");
   int pb = static_cast<int>((P + 255) / 256);
-  if (pb > 0) tok_count_kernel<<<pb, 256, 0, st>>>(P, ptok, T, cnt);
-  scan_excl_kernel<<<1, 1024, 0, st>>>(cnt, T, tptr);
-  if (pb > 0) tok_place_kernel<<<pb, 256, 0, st>>>(P, ptok, T, tptr, cursor, tpick);
-  tok_sort_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, tptr, tpick);
+  if (pb > 0) { tok_count_kernel<<<pb, 256, 0, st>>>(P, ptok, T, cnt); ::fsmoe::count_launch(); }
+  scan_excl_kernel<<<1, 1024, 0, st>>>(cnt, T, tptr); ::fsmoe::count_launch();
+  if (pb > 0) { tok_place_kernel<<<pb, 256, 0, st>>>(P, ptok, T, tptr, cursor, tpick); ::fsmoe::count_launch(); }
+  tok_sort_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, tptr, tpick); ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_token_index");
 }
 
@@ -423,15 +541,15 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
   if (row_bytes % 16 == 0) {
     dispatch_kernel<uint4><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 16), E, C,
                                                  chunks, pick_of_slot, ptok,
-                                                 static_cast<const uint4*>(x), static_cast<uint4*>(buf));
+                                                 static_cast<const uint4*>(x), static_cast<uint4*>(buf)); ::fsmoe::count_launch();
   } else if (row_bytes % 8 == 0) {
     dispatch_kernel<uint2><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 8), E, C,
                                                  chunks, pick_of_slot, ptok,
-                                                 static_cast<const uint2*>(x), static_cast<uint2*>(buf));
+                                                 static_cast<const uint2*>(x), static_cast<uint2*>(buf)); ::fsmoe::count_launch();
   } else {
     dispatch_kernel<uint16_t><<<grid, 256, 0, st>>>(
         n_slots, static_cast<int>(row_bytes / 2), E, C, chunks, pick_of_slot, ptok,
-        static_cast<const uint16_t*>(x), static_cast<uint16_t*>(buf));
+        static_cast<const uint16_t*>(x), static_cast<uint16_t*>(buf)); ::fsmoe::count_launch();
   }
   return cuda_status(cudaGetLastError(), "fsmoe_dispatch");
 }
@@ -443,8 +561,13 @@ int combine_launch(int dtype, int T, int M, int E, long long C, int chunks, cons
   const int grid = (T + 7) / 8;
   int rc = by_dtype(dtype, [&](auto tag) {
     using Tt = decltype(tag);
-    combine_kernel<Tt><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick, pw,
-                                             static_cast<const Tt*>(buf), static_cast<Tt*>(y));
+    if (M % CV == 0)
+      combine_kernel<Tt, true><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+                                                     pw, static_cast<const Tt*>(buf), static_cast<Tt*>(y));
+    else
+      combine_kernel<Tt, false><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+                                                      pw, static_cast<const Tt*>(buf), static_cast<Tt*>(y));
+    ::fsmoe::count_launch();
   });
   if (rc) return config_error("combine: unknown dtype");
   return cuda_status(cudaGetLastError(), "fsmoe_combine");
@@ -457,9 +580,15 @@ int dispatch_bwd_launch(int dtype, int T, int M, int E, long long C, int chunks,
   const int grid = (T + 7) / 8;
   int rc = by_dtype(dtype, [&](auto tag) {
     using Tt = decltype(tag);
-    dispatch_bwd_kernel<Tt><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
-                                                  static_cast<const Tt*>(dbuf),
-                                                  static_cast<Tt*>(dx), accumulate);
+    if (M % CV == 0)
+      dispatch_bwd_kernel<Tt, true><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+                                                          static_cast<const Tt*>(dbuf),
+                                                          static_cast<Tt*>(dx), accumulate);
+    else
+      dispatch_bwd_kernel<Tt, false><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+                                                           static_cast<const Tt*>(dbuf),
+                                                           static_cast<Tt*>(dx), accumulate);
+    ::fsmoe::count_launch();
   });
   if (rc) return config_error("dispatch_bwd: unknown dtype");
   return cuda_status(cudaGetLastError(), "fsmoe_dispatch_bwd");
@@ -474,10 +603,17 @@ int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long lo
   const int grid = static_cast<int>((n_slots + 7) / 8);
   int rc = by_dtype(dtype, [&](auto tag) {
     using Tt = decltype(tag);
-    combine_bwd_kernel<Tt><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
-                                                 static_cast<const Tt*>(dy),
-                                                 static_cast<const Tt*>(buf),
-                                                 static_cast<Tt*>(dbuf), dw);
+    if (M % CV == 0)
+      combine_bwd_kernel<Tt, true><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
+                                                         static_cast<const Tt*>(dy),
+                                                         static_cast<const Tt*>(buf),
+                                                         static_cast<Tt*>(dbuf), dw);
+    else
+      combine_bwd_kernel<Tt, false><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
+                                                          static_cast<const Tt*>(dy),
+                                                          static_cast<const Tt*>(buf),
+                                                          static_cast<Tt*>(dbuf), dw);
+    ::fsmoe::count_launch();
   });
   if (rc) return config_error("combine_bwd: unknown dtype");
   return cuda_status(cudaGetLastError(), "fsmoe_combine_bwd");
