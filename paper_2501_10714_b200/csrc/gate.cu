@@ -20,7 +20,9 @@
 // Compiled with --fmad=false: no multiply-add is ever contracted.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "capi_common.h"
 #include "kernels.h"
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(RD_THREADS)
                   int groups_a) {
   using ST = typename Stage<DT>::T;
   constexpr int JC = Stage<DT>::JC;
-  __shared__ __align__(16) ST xs[JC][RD_THREADS];
+  __shared__ ST xs[JC][RD_THREADS + 1];  // +1: conflict-free transposed stores
   __shared__ __align__(16) double ws[JC][RD_CG];
   const bool second = static_cast<int>(blockIdx.y) >= groups_a;
   const RowdotJob& J = second ? jb : ja;
@@ -76,9 +78,11 @@ __global__ void __launch_bounds__(RD_THREADS)
       int c = c0 + cc;
       ws[jj][cc] = (jj < jn && c < J.NC) ? J.W[(j0 + jj) * J.wsj + c * J.wsc] : 0.0;
     }
-    if (t < T) {
-      const long long base = static_cast<long long>(t) * M + j0;
-      for (int jj = 0; jj < jn; ++jj) xs[jj][threadIdx.x] = static_cast<ST>(load_as_double<DT>(x, base + jj));
+    // coalesced: consecutive threads read consecutive columns of one token row
+    for (int i = threadIdx.x; i < RD_THREADS * JC; i += RD_THREADS) {
+      const int tt = i / JC, jj = i % JC;
+      if (jj < jn && t0 + tt < T)
+        xs[jj][tt] = static_cast<ST>(load_as_double<DT>(x, static_cast<long long>(t0 + tt) * M + j0 + jj));
     }
     __syncthreads();
     if (t < T) {
@@ -429,6 +433,10 @@ int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
     rowdot2(RowdotJob{W, wsj, wsc, NC, out, ost, osc}, RowdotJob{nullptr, 0, 0, 0, nullptr, 0, 0});
   };
   (void)ws_bytes;
+  const bool exhaustive = getenv("FSMOE_GATE_EXHAUSTIVE") != nullptr;
+  if (!exhaustive && gate_prune_applicable(d))
+    return gate_prune_launch(d, x, w_score, w_noise, pick_token, pick_expert, pick_weight,
+                             scores_out, noise_out, spread_out, ws, st);
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
       double* raw = take(sizeof(double) * T * E);
@@ -472,9 +480,10 @@ int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
 size_t gate_workspace_bytes(const fsmoe_gate_desc& d) {
   const size_t T = d.tokens > 0 ? d.tokens : 0, E = d.score_cols > 0 ? d.score_cols : 0;
   auto r = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t prune = gate_prune_applicable(d) ? gate_prune_workspace_bytes(d) : 0;
   switch (d.kind) {
-    case FSMOE_GATE_NOISY_TOPK: return r(8 * T * E) * 2;
-    case FSMOE_GATE_SIGMOID_TOPK: return r(8 * T * E);
+    case FSMOE_GATE_NOISY_TOPK: return std::max(r(8 * T * E) * 2, prune);
+    case FSMOE_GATE_SIGMOID_TOPK: return std::max(r(8 * T * E), prune);
     case FSMOE_GATE_COSINE_TOPK: return r(8 * T * (d.proj_rows > 0 ? d.proj_rows : 0)) + r(8 * E);
     case FSMOE_GATE_EXPERT_CHOICE: return r(8 * T * E);
     default: return 0;

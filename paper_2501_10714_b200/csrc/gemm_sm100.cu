@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.h"
@@ -30,14 +31,9 @@ using namespace fsmoe_dev;
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 64;
-constexpr int STAGES = 4;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int NUM_THREADS = 384;
 constexpr int EPI_THREADS = 256;  // 8 epilogue warps
 constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 struct KParams {
   int kind;  // GemmKind
@@ -132,141 +128,196 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
   }
 }
 
+// CTAS = 1: one CTA computes a 128 x 256 tile (tcgen05 cta_group::1).
+// CTAS = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
+// with cta_group::2: each CTA stages its 128 rows of A and 128 of the 256
+// B rows; the leader issues the MMAs and both TMEMs hold their 128 rows.
+template <int CTAS>
+struct TileCfg {
+  static constexpr int BM = 128 * CTAS;      // tile rows (whole pair)
+  static constexpr int BN_CTA = BN / CTAS;   // B rows staged per CTA
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = BN_CTA * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int NSTAGE = CTAS == 1 ? 4 : 6;
+  static constexpr int SMEM = NSTAGE * STAGE + 1024 + 256;
+};
+
+template <int CTAS>
+__device__ __forceinline__ TileInfo decode_tile_c(const KParams& p, int t) {
+  TileInfo ti;
+  int per_g = p.m_tiles * p.n_tiles;
+  ti.g = t / per_g;
+  int rem = t - ti.g * per_g;
+  ti.mt = rem / p.n_tiles;
+  ti.nt = rem - ti.mt * p.n_tiles;
+  ti.skip = p.kind == 0 && ti.mt * TileCfg<CTAS>::BM >= valid_of(p, ti.g);
+  return ti;
+}
+
+template <int CTAS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const KParams p) {
+  using Cfg = TileCfg<CTAS>;
+  constexpr int NS = Cfg::NSTAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;   // [2]
-  uint64_t* tempty_bar = tfull_bar + 2;       // [2]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + NS * Cfg::STAGE);
+  uint64_t* empty_bar = full_bar + NS;
+  uint64_t* tfull_bar = empty_bar + NS;   // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const int warp = threadIdx.x / 32;
   const bool a_mn = (p.kind == 1);
   const bool b_mn = (p.kind == 1) || p.b_mn;
+  const uint32_t rank = CTAS == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CTAS;          // tile-scheduling unit (CTA or pair)
+  const int nunits = gridDim.x / CTAS;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], EPI_THREADS);
+      mbar_init(&tempty_bar[a], (EPI_THREADS / 32) * CTAS);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CTAS == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    else tmem_alloc<TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (every CTA loads its half) ==========
     if (elect_one()) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        TileInfo ti = decode_tile(p, t);
+      const int arow = static_cast<int>(rank) * 128;          // this CTA's A rows in the tile
+      const int brow = static_cast<int>(rank) * Cfg::BN_CTA;  // this CTA's B rows in the tile
+      auto issue = [&](uint8_t* dst, const CUtensorMap* m, int c0, int c1, int c2) {
+        if constexpr (CTAS == 2) tma_load_3d_pair(dst, m, mapa_shared(&full_bar[s], 0), c0, c1, c2);
+        else tma_load_3d(dst, m, &full_bar[s], c0, c1, c2);
+      };
+      auto begin_stage = [&]() {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        if (leader) mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE * CTAS);
+      };
+      for (int t = unit; t < p.num_tiles; t += nunits) {
+        TileInfo ti = decode_tile_c<CTAS>(p, t);
         if (ti.skip) continue;
         if (p.kind == 0) {
           const int nkb = ceil_div(p.K, BK);
           const int w = ti.g % p.n_w;
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&empty_bar[s], ph ^ 1);
-            uint8_t* sa = smem + s * STAGE_BYTES;
-            uint8_t* sb = sa + A_STAGE_BYTES;
-            mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
-            tma_load_3d(sa, &tmA, &full_bar[s], kb * BK, p.row0 + ti.mt * BM, ti.g);
+            begin_stage();
+            uint8_t* sa = smem + s * Cfg::STAGE;
+            uint8_t* sb = sa + Cfg::A_BYTES;
+            issue(sa, &tmA, kb * BK, p.row0 + ti.mt * Cfg::BM + arow, ti.g);
             if (!b_mn) {
-              tma_load_3d(sb, &tmB, &full_bar[s], kb * BK, ti.nt * BN, w);
+              issue(sb, &tmB, kb * BK, ti.nt * BN + brow, w);
             } else {
 #pragma unroll
-              for (int i = 0; i < BN / 64; ++i)
-                tma_load_3d(sb + i * 8192, &tmB, &full_bar[s], ti.nt * BN + i * 64, kb * BK, w);
+              for (int i = 0; i < Cfg::BN_CTA / 64; ++i)
+                issue(sb + i * 8192, &tmB, ti.nt * BN + brow + i * 64, kb * BK, w);
             }
-            if (++s == STAGES) { s = 0; ph ^= 1; }
+            if (++s == NS) { s = 0; ph ^= 1; }
           }
         } else {
           for (int b = ti.g; b < p.nblk; b += p.n_w) {
             const int nkb = kblocks_of_block(p, b);
             for (int kb = 0; kb < nkb; ++kb) {
-              mbar_wait(&empty_bar[s], ph ^ 1);
-              uint8_t* sa = smem + s * STAGE_BYTES;
-              uint8_t* sb = sa + A_STAGE_BYTES;
-              mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
+              begin_stage();
+              uint8_t* sa = smem + s * Cfg::STAGE;
+              uint8_t* sb = sa + Cfg::A_BYTES;
 #pragma unroll
-              for (int i = 0; i < BM / 64; ++i)
-                tma_load_3d(sa + i * 8192, &tmA, &full_bar[s], ti.mt * BM + i * 64, p.row0 + kb * BK, b);
+              for (int i = 0; i < 2; ++i)
+                issue(sa + i * 8192, &tmA, ti.mt * Cfg::BM + arow + i * 64, p.row0 + kb * BK, b);
 #pragma unroll
-              for (int i = 0; i < BN / 64; ++i)
-                tma_load_3d(sb + i * 8192, &tmB, &full_bar[s], ti.nt * BN + i * 64, p.row0 + kb * BK, b);
-              if (++s == STAGES) { s = 0; ph ^= 1; }
+              for (int i = 0; i < Cfg::BN_CTA / 64; ++i)
+                issue(sb + i * 8192, &tmB, ti.nt * BN + brow + i * 64, p.row0 + kb * BK, b);
+              if (++s == NS) { s = 0; ph ^= 1; }
             }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    const uint32_t idesc = make_idesc_bf16(BM, BN, a_mn, b_mn);
-    int s = 0;
-    uint32_t ph = 0;
-    int acc = 0;
-    uint32_t aph = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      TileInfo ti = decode_tile(p, t);
-      if (ti.skip) continue;
-      const int nkb = total_kblocks(p, ti.g);
-      mbar_wait(&tempty_bar[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t dtmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full_bar[s], ph);
+    // ===================== MMA issuer (leader CTA) =====================
+    if (leader) {
+      const uint32_t idesc = make_idesc_bf16(Cfg::BM, BN, a_mn, b_mn);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int t = unit; t < p.num_tiles; t += nunits) {
+        TileInfo ti = decode_tile_c<CTAS>(p, t);
+        if (ti.skip) continue;
+        const int nkb = total_kblocks(p, ti.g);
+        mbar_wait(&tempty_bar[acc], aph ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t sb = sa + A_STAGE_BYTES;
+        const uint32_t dtmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + s * Cfg::STAGE);
+            const uint32_t sb = sa + Cfg::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad = a_mn ? make_sdesc_sw128(sa + k * 2048, 8192, 1024)
-                               : make_sdesc_sw128(sa + k * 32, 16, 1024);
-            uint64_t bd = b_mn ? make_sdesc_sw128(sb + k * 2048, 8192, 1024)
-                               : make_sdesc_sw128(sb + k * 32, 16, 1024);
-            umma_bf16(dtmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              uint64_t ad = a_mn ? make_sdesc_sw128(sa + k * 2048, 8192, 1024)
+                                 : make_sdesc_sw128(sa + k * 32, 16, 1024);
+              uint64_t bd = b_mn ? make_sdesc_sw128(sb + k * 2048, 8192, 1024)
+                                 : make_sdesc_sw128(sb + k * 32, 16, 1024);
+              if constexpr (CTAS == 2) umma_bf16_pair(dtmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              else umma_bf16(dtmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            if constexpr (CTAS == 2) umma_commit_pair(&empty_bar[s], 0x3);
+            else umma_commit(&empty_bar[s]);
           }
-          umma_commit(&empty_bar[s]);
+          __syncwarp();
+          if (++s == NS) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) {
+          if (nkb > 0) {
+            if constexpr (CTAS == 2) umma_commit_pair(&tfull_bar[acc], 0x3);
+            else umma_commit(&tfull_bar[acc]);
+          } else {
+            for (int r = 0; r < CTAS; ++r) mbar_arrive_cluster(mapa_shared(&tfull_bar[acc], r));
+          }
         }
         __syncwarp();
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (++acc == 2) { acc = 0; aph ^= 1; }
       }
-      if (elect_one()) {
-        if (nkb > 0) umma_commit(&tfull_bar[acc]);
-        else mbar_arrive(&tfull_bar[acc]);
-      }
-      __syncwarp();
-      if (++acc == 2) { acc = 0; aph ^= 1; }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue =====================
+    // ===================== epilogue (every CTA: its 128 TMEM lanes) ========
     const int q = warp & 3;
     const int half = (warp - 4) >> 2;  // which 128 accumulator columns
     const int lane = threadIdx.x & 31;
+    const uint32_t tempty_leader = mapa_shared(&tempty_bar[0], 0);
     int acc = 0;
     uint32_t aph = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      TileInfo ti = decode_tile(p, t);
+    for (int t = unit; t < p.num_tiles; t += nunits) {
+      TileInfo ti = decode_tile_c<CTAS>(p, t);
       if (ti.skip) continue;
       const int nkb = total_kblocks(p, ti.g);
       mbar_wait(&tfull_bar[acc], aph);
       tc_fence_after();
-      const int row = ti.mt * BM + q * 32 + lane;  // within the processed window
+      const int row = ti.mt * Cfg::BM + static_cast<int>(rank) * 128 + q * 32 + lane;
       const bool row_ok = row < p.out_rows;
       const long long orow = p.kind == 0
                                  ? static_cast<long long>(ti.g) * p.rows_total + p.row0 + row
@@ -277,8 +328,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (p.epi == static_cast<int>(Epi::SwigluFwd)) {
         // tile cols: [0,128) gate units, [128,256) up units (same 128 units)
         __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-        __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) +
-                           orow * p.ldd2;
+        __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) + orow * p.ldd2;
         for (int c = 2 * half; c < 2 * half + 2; ++c) {
           float g[32];
           if (nkb > 0) {
@@ -295,7 +345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 32; ++i) g[i] = v[i] = 0.f;
           }
           const int gcol = ti.nt * BN + c * 32;
-          const int unit = ti.nt * (BN / 2) + c * 32;
+          const int hcol = ti.nt * (BN / 2) + c * 32;
           if (row_ok && gcol < p.out_cols) {
             store_bf16x32(Z + gcol, g);
             store_bf16x32(Z + gcol + 128, v);
@@ -306,7 +356,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               float ub = bf2f(__float2bfloat16(v[i]));
               h[i] = gb * sigmoid_f(gb) * ub;
             }
-            store_bf16x32(H + unit, h);
+            store_bf16x32(H + hcol, h);
           }
         }
       } else {
@@ -344,8 +394,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             case static_cast<int>(Epi::GeluFwd): {
               __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-              __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) +
-                                 orow * p.ldd2;
+              __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) + orow * p.ldd2;
               store_bf16x32(Z + col, v);
               float h[32];
 #pragma unroll
@@ -354,8 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               break;
             }
             case static_cast<int>(Epi::GeluBwd): {
-              const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) +
-                                       orow * p.ldz;
+              const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
               __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
               float z[32];
               load_bf16x32(Z + col, z);
@@ -365,10 +413,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               break;
             }
             case static_cast<int>(Epi::SwigluBwd): {
-              const int unit = col;
-              const int gcol = (unit / 128) * 256 + (unit % 128);
-              const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) +
-                                       orow * p.ldz;
+              const int gcol = (col / 128) * 256 + (col % 128);
+              const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
               __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
               float g[32], u[32], dg[32];
               load_bf16x32(Z + gcol, g);
@@ -390,16 +436,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CTAS == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    if constexpr (CTAS == 2) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+    else tmem_dealloc<TMEM_COLS>(tmem_base);
   }
 }
 
@@ -474,23 +526,33 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   if (p.row0 < 0 || p.row0 + pr.rows > p.rows_total || p.row0 % 64) return cudaErrorInvalidValue;
   if (pr.kind == GemmKind::KGrouped && p.row0 + pr.rows < p.rows_total && pr.rows % 64)
     return cudaErrorInvalidValue;  // the K window must end on a 64-row boundary
+  // Tile shape: CTA pairs (256 x 256, cta_group::2) unless the problem is too
+  // small to give every SM pair work; FSMOE_GEMM_CTAS=1|2 forces a variant.
+  const int units_rows = pr.kind == GemmKind::RowGrouped ? pr.rows : pr.Mo;
+  const int units_cols = pr.kind == GemmKind::RowGrouped ? pr.N : pr.No;
+  const int groups = pr.kind == GemmKind::RowGrouped ? pr.nblk : p.n_w;
+  long long pair_tiles = static_cast<long long>(groups) * ((units_rows + 255) / 256) *
+                         ((units_cols + BN - 1) / BN);
+  int ctas = pair_tiles >= num_sms() / 4 ? 2 : 1;
+  if (const char* env = getenv("FSMOE_GEMM_CTAS")) ctas = atoi(env) == 1 ? 1 : 2;
+  const int bm = 128 * ctas, bn_cta = BN / ctas;
   if (pr.kind == GemmKind::RowGrouped) {
     if (pr.K % 8 || pr.N % 64 || pr.K <= 0 || pr.N <= 0) return cudaErrorInvalidValue;
-    p.m_tiles = (pr.rows + BM - 1) / BM;
+    p.m_tiles = (pr.rows + bm - 1) / bm;
     p.n_tiles = (pr.N + BN - 1) / BN;
     p.n_groups = pr.nblk;
     p.out_rows = pr.rows;
     // SwigluBwd's output columns are the interleaved dZ (2N); masking is on N units.
     p.out_cols = pr.N;
-    if (!make_map3(&ta, pr.A, pr.K, p.rows_total, pr.nblk, BK, BM)) return cudaErrorInvalidValue;
+    if (!make_map3(&ta, pr.A, pr.K, p.rows_total, pr.nblk, BK, 128)) return cudaErrorInvalidValue;
     if (!pr.b_mn_major) {
-      if (!make_map3(&tb, pr.B, pr.K, pr.N, p.n_w, BK, BN)) return cudaErrorInvalidValue;
+      if (!make_map3(&tb, pr.B, pr.K, pr.N, p.n_w, BK, bn_cta)) return cudaErrorInvalidValue;
     } else {
       if (!make_map3(&tb, pr.B, pr.N, pr.K, p.n_w, 64, BK)) return cudaErrorInvalidValue;
     }
   } else {
     if (pr.Mo % 64 || pr.No % 64 || pr.nblk % p.n_w) return cudaErrorInvalidValue;
-    p.m_tiles = (pr.Mo + BM - 1) / BM;
+    p.m_tiles = (pr.Mo + bm - 1) / bm;
     p.n_tiles = (pr.No + BN - 1) / BN;
     p.n_groups = p.n_w;
     p.out_rows = pr.Mo;
@@ -501,12 +563,33 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.num_tiles = p.n_groups * p.m_tiles * p.n_tiles;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
+    cudaFuncSetAttribute(grouped_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TileCfg<1>::SMEM);
+    cudaFuncSetAttribute(grouped_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TileCfg<2>::SMEM);
     attr_set = true;
   }
-  int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
-  grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p); ::fsmoe::count_launch();
+  const int max_units = num_sms() / ctas;
+  const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
+  if (ctas == 1) {
+    grouped_gemm_kernel<1><<<units, NUM_THREADS, TileCfg<1>::SMEM, stream>>>(ta, tb, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(units * 2);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = TileCfg<2>::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<2>, ta, tb, p);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  ::fsmoe::count_launch();
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -16,6 +16,14 @@ int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
                 double* proj_out, int* d_status, void* ws, size_t ws_bytes, cudaStream_t st);
 void cosine_enorm(int P, int E, const double* w, double* en, cudaStream_t st);
 
+// Pruned exact selection for noisy/sigmoid gates (gate_prune.cu).
+bool gate_prune_applicable(const fsmoe_gate_desc& d);
+size_t gate_prune_workspace_bytes(const fsmoe_gate_desc& d);
+int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
+                      const double* w_noise, int* pick_token, int* pick_expert,
+                      double* pick_weight, double* scores_out, double* noise_out,
+                      double* spread_out, void* ws, cudaStream_t st);
+
 size_t gate_bwd_workspace_bytes(const fsmoe_gate_desc& d);
 int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
                     const double* w_noise, const double* proj, const int* ptok, const int* pexp,

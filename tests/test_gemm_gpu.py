@@ -19,6 +19,14 @@ def _ops():
     return ops
 
 
+@pytest.fixture(params=["1", "2"], autouse=True)
+def gemm_ctas(request, monkeypatch):
+    """Run every GEMM test on both tile variants: single-CTA 128x256 and the
+    CTA-pair 256x256 (tcgen05 cta_group::2)."""
+    monkeypatch.setenv("FSMOE_GEMM_CTAS", request.param)
+    return request.param
+
+
 def _rel(a, b):
     return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-30)).item()
 
@@ -80,8 +88,9 @@ def test_k_grouped_wgrad(precision, accumulate):
     assert _rel(D, ref) < (5e-3 if precision == 0 else 1e-5)
 
 
-def test_valid_rows_skip_and_kextent():
+def test_valid_rows_skip_and_kextent(gemm_ctas):
     ops = _ops()
+    tile = 128 * int(gemm_ctas)
     nblk, rows, K, N = 4, 512, 128, 256
     valid = torch.tensor([0, 100, 512, 300], device="cuda", dtype=torch.int64)
     A = _rand(nblk, rows, K)
@@ -93,7 +102,7 @@ def test_valid_rows_skip_and_kextent():
     torch.cuda.synchronize()
     for b in range(nblk):
         v = int(valid[b])
-        vr = (v + 127) // 128 * 128  # computed tiles cover whole 128-row tiles
+        vr = min((v + tile - 1) // tile * tile, rows)  # computed tiles cover whole row tiles
         ref = A[b, :vr].double() @ B[b].double().T
         if vr:
             assert _rel(D[b, :vr], ref) < 2e-2
@@ -193,3 +202,31 @@ def test_large_perf_smoke():
     print(f"\n[gemm] E{E} C{C} M{M} H{H}: {ms*1e3:.1f} us  {tflops:.0f} TFLOP/s")
     ref = X[3].float() @ W1[3].float().T
     assert _rel(Z[3], ref) < 2e-2
+
+
+@pytest.mark.parametrize("kind", ["row", "k"])
+def test_row_window_chunks(kind):
+    """Pipeline chunks: rows [row0, row0+rows) of blocks holding rows_total rows."""
+    ops = _ops()
+    nblk, C, K, N = 4, 640, 256, 512
+    A = _rand(nblk, C, K)
+    if kind == "row":
+        B = _rand(nblk, N, K, scale=K ** -0.5)
+        D = torch.full((nblk, C, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+        for lo, hi in [(0, 256), (256, 512), (512, 640)]:
+            ops.grouped_gemm("row", A, B, D, nblk=nblk, rows=hi - lo, rows_total=C, row0=lo, K=K,
+                             N=N, n_w=nblk)
+        torch.cuda.synchronize()
+        ref = torch.stack([A[b].double() @ B[b].double().T for b in range(nblk)])
+        assert _rel(D, ref) < 2e-2
+    else:
+        G = _rand(nblk, C, N)
+        W = torch.zeros(2, K, N, device="cuda")
+        for i, (lo, hi) in enumerate([(0, 256), (256, 512), (512, 640)]):
+            ops.grouped_gemm("k", A, G, W, nblk=nblk, rows=hi - lo, rows_total=C, row0=lo, Mo=K,
+                             No=N, n_w=2, epi="store_f32", accumulate=i > 0)
+        torch.cuda.synchronize()
+        ref = torch.zeros(2, K, N, dtype=torch.float64, device="cuda")
+        for b in range(nblk):
+            ref[b % 2] += A[b].double().T @ G[b].double()
+        assert _rel(W, ref) < 5e-3

@@ -1,0 +1,41 @@
+"""Run the six expert-FFN GEMM launches of one bench step (BASELINE configs[1]
+shape, E=16, C=1024, M=1024, H=4096) once each — the target of the ncu
+--set full capture in profiles/."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2501_10714_b200 import ops  # noqa: E402
+
+
+def main(reps=1, ffn="simple"):
+    E, C, M, H = 16, 1024, 1024, 4096
+    N1 = H if ffn == "simple" else 2 * H
+    bf = torch.bfloat16
+    X = torch.randn(E, C, M, device="cuda").to(bf)
+    W1 = (torch.randn(E, N1, M, device="cuda") / 32).to(bf)
+    W2 = (torch.randn(E, M, H, device="cuda") / 64).to(bf)
+    Z = torch.empty(E, C, N1, device="cuda", dtype=bf)
+    Hh = torch.empty(E, C, H, device="cuda", dtype=bf)
+    O = torch.empty(E, C, M, device="cuda", dtype=bf)
+    dO = torch.randn(E, C, M, device="cuda").to(bf)
+    dX = torch.empty_like(O)
+    gw1 = torch.empty(E, N1, M, device="cuda")
+    gw2 = torch.empty(E, M, H, device="cuda")
+    for _ in range(reps):
+        ops.grouped_gemm("row", X, W1, Z, nblk=E, rows=C, K=M, N=N1, n_w=E,
+                         epi="gelu_fwd" if ffn == "simple" else "swiglu_fwd", D2=Hh, ldd2=H)
+        ops.grouped_gemm("row", Hh, W2, O, nblk=E, rows=C, K=H, N=M, n_w=E)
+        ops.grouped_gemm("k", dO, Hh, gw2, nblk=E, rows=C, Mo=M, No=H, n_w=E, epi="store_f32")
+        ops.grouped_gemm("row", dO, W2, Z, nblk=E, rows=C, K=M, N=H, n_w=E, b_mn_major=True,
+                         epi="gelu_bwd" if ffn == "simple" else "swiglu_bwd", Zin=Z, ldz=N1, ldd=N1)
+        ops.grouped_gemm("k", Z, X, gw1, nblk=E, rows=C, Mo=N1, No=M, n_w=E, epi="store_f32")
+        ops.grouped_gemm("row", Z, W1, dX, nblk=E, rows=C, K=N1, N=M, n_w=E, b_mn_major=True)
+    torch.cuda.synchronize()
+    print("ok")
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 1)
