@@ -1,26 +1,30 @@
 // gate_prune.cu — K1 fast path for the linear-score gates (noisy_topk,
 // sigmoid_topk): exact selection without computing every fp64 logit.
 //
-//  1. approx_scores_kernel: fp32 FMA scores s~ = x . W for all (token,
-//     column) (W_g and, for noisy, W_noise), a SIMT tile GEMM.
-//  2. prune_select_kernel (one warp per token):
-//       * rigorous bound |s~ - s_ref| <= B = c * |x_t|_2 * |W_e|_2 with
-//         c = (M+4) 2^-24 (1.01) + (M+2) 2^-53, covering fp32 rounding of x, W
-//         and the FMA chain, and the reference's own fp64 sequential rounding
-//         (s_ref = matvec_row of workload.cpp:103-108);
-//       * noisy: s = raw + n * softplus(spread) with the exact per-token
-//         mt19937_64 Box-Muller noise n (workload.cpp:85-99, 183-186);
-//         softplus is 1-Lipschitz, so B_s = B_raw + |n| B_spread;
-//       * candidates = experts whose upper bound reaches the k-th largest lower
-//         bound — provably a superset of the exact top-k;
-//       * exact fp64 logits (sequential j, no FMA) only for the candidates,
-//         exact top-k among them with ties to the lowest index (111-121),
-//         then the masked softmax (123-133) or logistic (198).
-//     Outputs are identical to the exhaustive path (tests/test_routing_gpu.py
-//     runs both against the reference's golden vectors).
+//  1. w_prep_kernel       W in fp32 [M][NC] (approximate phase), W^T in fp64
+//                         [NC][M] (exact phase), column norms.
+//  2. approx_scores_kernel  s~ = x . W for all (token, column), fp32 FMA
+//                         SIMT tiles split over K, plus |x_t|^2 in fp64.
+//  3. mt_kernel (thread per token): the first 2E outputs of
+//     mt19937_64(seed + t) (workload.cpp:85-99, 184).
+//  4. bound_kernel (thread per token x expert): Box-Muller noise, s~ and the
+//     rigorous bound |s~ - s_ref| <= B = c |x_t|_2 |W_e|_2 with
+//     c = (M+8+4) 2^-24 (1.01) + (M+2) 2^-53, covering fp32 rounding of x, W,
+//     the FMA chain and split partial sums, and the reference's own fp64
+//     sequential rounding (matvec_row, 103-108); for noisy, softplus is
+//     1-Lipschitz: B_s = B_raw + |n| B_spread.
+//  5. cand_kernel (thread per token): candidates = experts whose upper bound
+//     reaches the k-th largest lower bound — a provable superset of the exact
+//     top-k — appended to per-expert lists.
+//  6. exact_kernel (thread per candidate, warps share an expert): the
+//     reference's fp64 logits (sequential j, separately rounded mul/add).
+//  7. final_kernel (thread per token): exact top-k among candidates with ties
+//     to the lowest index (111-121), masked softmax (123-133) or logistic
+//     (198), picks token-major, saved tensors for the backward.
+// Results are identical to the exhaustive path; tests/test_routing_gpu.py runs
+// both against the reference's golden vectors.
 //
-// Compiled with --fmad=false (the exact logits must not contract; the
-// approximate phase uses explicit fmaf).
+// Compiled with --fmad=false (explicit fmaf where the approximation wants it).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -29,26 +33,33 @@
 #include "capi_common.h"
 #include "kernels.h"
 #include "route_common.cuh"
+#include "sm100.cuh"
 
 namespace fsmoe {
 namespace {
 
 using namespace fsmoe_dev;
 
-constexpr int AP_TOK = 64;   // tokens per block
-constexpr int AP_COL = 32;   // columns per block
-constexpr int AP_JC = 32;    // reduction chunk
+constexpr int PS_MAXE = 64;  // experts handled by this path
 
-// W32[j][c] = (float)W_a[j][c] (c < Ea) | (float)W_b[j][c - Ea]; wn[c] = |column|_2.
-__global__ void w_to_f32_kernel(int M, int Ea, const double* __restrict__ Wa, int Eb,
-                                const double* __restrict__ Wb, float* __restrict__ W32,
-                                double* __restrict__ wn) {
+template <int DT>
+__device__ __forceinline__ float load_as_float(const void* base, long long i) {
+  if constexpr (DT == 2) return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]);
+  else if constexpr (DT == 1) return static_cast<const float*>(base)[i];
+  else return static_cast<float>(static_cast<const double*>(base)[i]);
+}
+
+// W32[j][c], WT[c][j] for c < Ea from Wa, else from Wb; wn[c] = |column|_2 (upper bound).
+__global__ void w_prep_kernel(int M, int Ea, const double* __restrict__ Wa, int Eb,
+                              const double* __restrict__ Wb, float* __restrict__ W32,
+                              double* __restrict__ WT, double* __restrict__ wn) {
   const int NC = Ea + Eb;
   const int c = blockIdx.x;
   double ss = 0.0;
   for (int j = threadIdx.x; j < M; j += blockDim.x) {
     double v = c < Ea ? Wa[static_cast<long long>(j) * Ea + c] : Wb[static_cast<long long>(j) * Eb + (c - Ea)];
     W32[static_cast<long long>(j) * NC + c] = static_cast<float>(v);
+    WT[static_cast<long long>(c) * M + j] = v;
     ss = __fma_rn(v, v, ss);
   }
   __shared__ double red[32];
@@ -62,48 +73,72 @@ __global__ void w_to_f32_kernel(int M, int Ea, const double* __restrict__ Wa, in
   }
 }
 
-// out[t][c] = sum_j x[t][j] * W32[j][c]  (fp32 FMA); 64 tokens x 32 cols per
-// block, 256 threads, each 2 tokens x 4 columns.
+constexpr int AP_TOK = 32;   // tokens per block
+constexpr int AP_COL = 32;   // columns per block
+constexpr int AP_JC = 64;    // reduction chunk
+constexpr int AP_KS = 8;     // reduction splits (partials summed by bound_kernel)
+
+// part[ks][t][c] = sum_{j in split ks} x[t][j] * W32[j][c] (fp32 FMA); 32 tokens
+// x 32 cols per block of 64 threads (4 tokens x 4 cols each), gridDim.z = K
+// splits. blockIdx.y == 0 also writes the split's |x_t|^2 (fp64).
 template <int DT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(64)
     approx_scores_kernel(const void* __restrict__ x, int T, int M, const float* __restrict__ W32,
-                         int NC, float* __restrict__ out) {
-  __shared__ float xs[AP_JC][AP_TOK + 1];
+                         int NC, float* __restrict__ part, double* __restrict__ xn2part) {
+  __shared__ __align__(16) float xs[AP_JC][AP_TOK + 4];  // transposed: 4 tokens = one float4
   __shared__ __align__(16) float ws[AP_JC][AP_COL];
   const int t0 = blockIdx.x * AP_TOK, c0 = blockIdx.y * AP_COL;
-  const int ty = threadIdx.x / 8, tx = threadIdx.x % 8;  // 32 token pairs x 8 column quads
-  float acc[2][4] = {};
-  for (int j0 = 0; j0 < M; j0 += AP_JC) {
+  const int ks = blockIdx.z;
+  const int span = ((M + AP_KS - 1) / AP_KS + AP_JC - 1) / AP_JC * AP_JC;
+  const int jbeg = ks * span, jend = min(M, jbeg + span);
+  const int ty = threadIdx.x / 8, tx = threadIdx.x % 8;  // 8 token quads x 8 column quads
+  float acc[4][4] = {};
+  double nrm = 0.0;
+  for (int j0 = jbeg; j0 < jend; j0 += AP_JC) {
     __syncthreads();
-    for (int i = threadIdx.x; i < AP_TOK * AP_JC; i += 256) {
-      int tt = i / AP_JC, jj = i % AP_JC;
-      int t = t0 + tt, j = j0 + jj;
-      xs[jj][tt] = (t < T && j < M) ? static_cast<float>(load_as_double<DT>(x, static_cast<long long>(t) * M + j)) : 0.f;
+#pragma unroll
+    for (int i = threadIdx.x; i < AP_TOK * AP_JC; i += 64) {
+      const int tt = i / AP_JC, jj = i % AP_JC;
+      const int t = t0 + tt, j = j0 + jj;
+      xs[jj][tt] = (t < T && j < jend) ? load_as_float<DT>(x, static_cast<long long>(t) * M + j) : 0.f;
     }
-    for (int i = threadIdx.x; i < AP_JC * AP_COL; i += 256) {
-      int jj = i / AP_COL, cc = i % AP_COL;
-      int j = j0 + jj, c = c0 + cc;
-      ws[jj][cc] = (j < M && c < NC) ? W32[static_cast<long long>(j) * NC + c] : 0.f;
+#pragma unroll
+    for (int i = threadIdx.x; i < AP_JC * AP_COL; i += 64) {
+      const int jj = i / AP_COL, cc = i % AP_COL;
+      const int j = j0 + jj, c = c0 + cc;
+      ws[jj][cc] = (j < jend && c < NC) ? W32[static_cast<long long>(j) * NC + c] : 0.f;
     }
     __syncthreads();
+    if (blockIdx.y == 0 && threadIdx.x < AP_TOK)
+      for (int jj = 0; jj < AP_JC; ++jj) {
+        const double v = xs[jj][threadIdx.x];
+        nrm = __fma_rn(v, v, nrm);
+      }
 #pragma unroll 8
     for (int jj = 0; jj < AP_JC; ++jj) {
-      const float a0 = xs[jj][2 * ty], a1 = xs[jj][2 * ty + 1];
+      const float4 av = reinterpret_cast<const float4*>(xs[jj])[ty];
+      const float a[4] = {av.x, av.y, av.z, av.w};
       const float4 w = reinterpret_cast<const float4*>(ws[jj])[tx];
-      acc[0][0] = fmaf(a0, w.x, acc[0][0]); acc[0][1] = fmaf(a0, w.y, acc[0][1]);
-      acc[0][2] = fmaf(a0, w.z, acc[0][2]); acc[0][3] = fmaf(a0, w.w, acc[0][3]);
-      acc[1][0] = fmaf(a1, w.x, acc[1][0]); acc[1][1] = fmaf(a1, w.y, acc[1][1]);
-      acc[1][2] = fmaf(a1, w.z, acc[1][2]); acc[1][3] = fmaf(a1, w.w, acc[1][3]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] = fmaf(a[i], w.x, acc[i][0]);
+        acc[i][1] = fmaf(a[i], w.y, acc[i][1]);
+        acc[i][2] = fmaf(a[i], w.z, acc[i][2]);
+        acc[i][3] = fmaf(a[i], w.w, acc[i][3]);
+      }
     }
   }
+  if (blockIdx.y == 0 && threadIdx.x < AP_TOK && t0 + threadIdx.x < T)
+    xn2part[static_cast<long long>(ks) * T + t0 + threadIdx.x] = nrm;
+  float* out = part + static_cast<long long>(ks) * T * NC;
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    const int t = t0 + 2 * ty + a;
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + 4 * ty + i;
     if (t >= T) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int c = c0 + 4 * tx + b;
-      if (c < NC) out[static_cast<long long>(t) * NC + c] = acc[a][b];
+      if (c < NC) out[static_cast<long long>(t) * NC + c] = acc[i][b];
     }
   }
 }
@@ -122,237 +157,423 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
   return y;
 }
 
-// Normal draw of expert e for mt19937_64(seed): outputs 2e and 2e+1
-// (requires 2e + 1 < 156: words 2e..2e+2 and 156+2e..157+2e of the seeding).
-__device__ double noise_of(uint64_t seed, int e) {
-  const int i0 = 2 * e;
-  uint64_t w = seed, a = 0, b = 0, c = 0, d = 0, f = 0;
-  if (i0 == 0) a = w;
-  for (int i = 1; i <= 157 + i0; ++i) {
-    w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
-    if (i == i0) a = w;
-    if (i == i0 + 1) b = w;
-    if (i == i0 + 2) c = w;
-    if (i == 156 + i0) d = w;
-    if (i == 157 + i0) f = w;
-  }
-  uint64_t y0 = (a & MT_UM) | (b & MT_LM);
-  uint64_t o0 = temper(d ^ (y0 >> 1) ^ ((y0 & 1ULL) ? MT_A : 0ULL));
-  uint64_t y1 = (b & MT_UM) | (c & MT_LM);
-  uint64_t o1 = temper(f ^ (y1 >> 1) ^ ((y1 & 1ULL) ? MT_A : 0ULL));
-  double u1 = __dmul_rn(__dadd_rn(static_cast<double>(o0 >> 11), 0.5), 0x1.0p-53);
-  double u2 = __dmul_rn(__dadd_rn(static_cast<double>(o1 >> 11), 0.5), 0x1.0p-53);
-  double two_pi = 2.0 * 3.141592653589793238462643383279502884;
-  return __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
-}
-
-// Sequential fp64 dot (matvec_row order, separately rounded mul/add).
-template <int DT>
-__device__ double exact_dot(const void* x, long long xrow, int M, const double* W, int ldw, int c) {
-  double acc = 0.0;
-#pragma unroll 8
-  for (int j = 0; j < M; ++j)
-    acc = __dadd_rn(acc, __dmul_rn(load_as_double<DT>(x, xrow + j), W[static_cast<long long>(j) * ldw + c]));
-  return acc;
-}
-
-constexpr int PS_MAXE = 64;           // experts per token on this path
-constexpr int PS_PER = PS_MAXE / 32;  // experts per lane
-
-// KIND 0: noisy_topk, 1: sigmoid_topk. One warp per token.
-template <int DT, int KIND>
-__global__ void __launch_bounds__(256)
-    prune_select_kernel(const void* __restrict__ x, int T, int M, int E, int k, uint64_t seed,
-                        const float* __restrict__ approx, const double* __restrict__ wn,
-                        double cB, const double* __restrict__ Wg, const double* __restrict__ Wn,
-                        int* __restrict__ pick_token, int* __restrict__ pick_expert,
-                        double* __restrict__ pick_weight, double* __restrict__ scores_out,
-                        double* __restrict__ noise_out, double* __restrict__ spread_out) {
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+// First 2E outputs of std::mt19937_64(seed+t) (2E <= 156: output i needs seed
+// words i, i+1, i+156 — libstdc++ twists the whole state on the first draw).
+// One thread per token: the seeding recurrence is sequential.
+template <int MAXE>
+__global__ void __launch_bounds__(128)
+    mt_kernel(int T, int E, uint64_t seed, uint64_t* __restrict__ draws) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
-  const int lane = threadIdx.x & 31;
-  const long long xrow = static_cast<long long>(t) * M;
+  uint64_t lo[2 * MAXE + 1];
+  uint64_t w = seed + static_cast<uint64_t>(t);
+  lo[0] = w;
+  const int nout = 2 * E;
+  for (int i = 1; i <= nout; ++i) {
+    w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+    lo[i] = w;
+  }
+  for (int i = nout + 1; i < 156; ++i) w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+  uint64_t* out = draws + static_cast<long long>(t) * nout;
+  for (int o = 0; o < nout; ++o) {
+    w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(156 + o);
+    const uint64_t y = (lo[o] & MT_UM) | (lo[o + 1] & MT_LM);
+    out[o] = temper(w ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL));
+  }
+}
+
+// One thread per (token, expert): Box-Muller noise (noisy), the approximate
+// score and its rigorous bound -> [lo, hi].
+template <int KIND>
+__global__ void __launch_bounds__(256)
+    bound_kernel(int T, int E, int M, const float* __restrict__ part, const double* __restrict__ xn2part,
+                 const double* __restrict__ wn, double cB, const uint64_t* __restrict__ draws,
+                 double* __restrict__ noise, double* __restrict__ sapx, double* __restrict__ spapx,
+                 double* __restrict__ lo, double* __restrict__ hi) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(T) * E) return;
+  const int t = static_cast<int>(i / E), e = static_cast<int>(i % E);
   const int NC = KIND == 0 ? 2 * E : E;
-
-  // |x_t|_2 (upper bound)
-  double ss = 0.0;
-  for (int j = lane; j < M; j += 32) {
-    double v = load_as_double<DT>(x, xrow + j);
-    ss = __fma_rn(v, v, ss);
+  double xn = 0.0;
+  float r = 0.f, sp = 0.f;
+  for (int ks = 0; ks < AP_KS; ++ks) {
+    xn += xn2part[static_cast<long long>(ks) * T + t];
+    const float* p = part + (static_cast<long long>(ks) * T + t) * NC;
+    r += p[e];
+    if (KIND == 0) sp += p[E + e];
   }
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const double xnorm = sqrt(ss) * (1.0 + 1e-12);
-
-  // approximate scores and bounds for this lane's experts
-  double sa[PS_PER], bnd[PS_PER], nz[PS_PER], spa[PS_PER];
-#pragma unroll
-  for (int i = 0; i < PS_PER; ++i) {
-    const int e = lane + 32 * i;
-    sa[i] = -1e300;
-    bnd[i] = 0.0;
-    nz[i] = 0.0;
-    spa[i] = 0.0;
-    if (e >= E) continue;
-    const double r = approx[static_cast<long long>(t) * NC + e];
-    const double br = cB * xnorm * wn[e];
-    if (KIND == 0) {
-      nz[i] = noise_of(seed + static_cast<uint64_t>(t), e);
-      spa[i] = approx[static_cast<long long>(t) * NC + E + e];
-      const double bs = cB * xnorm * wn[E + e];
-      const double sp = log1p(exp(spa[i]));
-      sa[i] = r + nz[i] * sp;
-      bnd[i] = br + fabs(nz[i]) * bs + 1e-12 * (fabs(r) + fabs(nz[i] * sp) + 1e-200);
-    } else {
-      sa[i] = r;
-      bnd[i] = br + 1e-12 * (fabs(r) + 1e-200);
-    }
+  // summing the AP_KS fp32 partials adds at most AP_KS more roundings: covered
+  // by the (M + 4) term since M >= AP_KS splits are never finer than 1 term.
+  const double xnorm = sqrt(xn) * (1.0 + 1e-12);
+  const double br = cB * xnorm * wn[e];
+  double s, b;
+  if (KIND == 0) {
+    const uint64_t o0 = draws[static_cast<long long>(t) * 2 * E + 2 * e];
+    const uint64_t o1 = draws[static_cast<long long>(t) * 2 * E + 2 * e + 1];
+    double u1 = __dmul_rn(__dadd_rn(static_cast<double>(o0 >> 11), 0.5), 0x1.0p-53);
+    double u2 = __dmul_rn(__dadd_rn(static_cast<double>(o1 >> 11), 0.5), 0x1.0p-53);
+    double two_pi = 2.0 * 3.141592653589793238462643383279502884;
+    const double n = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
+    const double bs = cB * xnorm * wn[E + e];
+    const double soft = log1p(exp(static_cast<double>(sp)));
+    s = static_cast<double>(r) + n * soft;
+    b = br + fabs(n) * bs + 1e-12 * (fabs(static_cast<double>(r)) + fabs(n * soft)) + 1e-300;
+    noise[i] = n;
+    spapx[i] = sp;
+  } else {
+    s = r;
+    b = br + 1e-12 * fabs(static_cast<double>(r)) + 1e-300;
   }
+  sapx[i] = s;
+  lo[i] = s - b;
+  hi[i] = s + b;
+}
 
-  // k-th largest lower bound (ties irrelevant: only its value is used)
+// One thread per token: candidates = experts whose upper bound reaches the
+// k-th largest lower bound; appended to per-expert lists.
+__global__ void __launch_bounds__(128)
+    cand_kernel(int T, int E, int k, const double* __restrict__ lo, const double* __restrict__ hi,
+                uint64_t* __restrict__ mask, int* __restrict__ lists, int* __restrict__ counts) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const double* l = lo + static_cast<long long>(t) * E;
+  const double* h = hi + static_cast<long long>(t) * E;
   uint64_t taken = 0;
-  double kth = -1e300;
+  double kth = 0.0;
   for (int j = 0; j < k; ++j) {
-    double best = -1e300;
     int bi = -1;
-#pragma unroll
-    for (int i = 0; i < PS_PER; ++i) {
-      const int e = lane + 32 * i;
-      if (e < E && !((taken >> e) & 1ULL) && (bi < 0 || sa[i] - bnd[i] > best)) {
-        best = sa[i] - bnd[i];
-        bi = e;
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) {
-        best = ob;
-        bi = oi;
-      }
-    }
+    for (int e = 0; e < E; ++e)
+      if (!((taken >> e) & 1ULL) && (bi < 0 || l[e] > l[bi])) bi = e;
     taken |= 1ULL << bi;
-    kth = best;
+    kth = l[bi];
   }
-
-  // exact logits for candidates
-  double sx[PS_PER];
-  uint64_t cand = 0;
-#pragma unroll
-  for (int i = 0; i < PS_PER; ++i) {
-    const int e = lane + 32 * i;
-    sx[i] = sa[i];
-    if (e >= E || sa[i] + bnd[i] < kth) continue;
-    cand |= 1ULL << e;
-    const double raw = exact_dot<DT>(x, xrow, M, Wg, E, e);
-    if (KIND == 0) {
-      const double spread = exact_dot<DT>(x, xrow, M, Wn, E, e);
-      spa[i] = spread;
-      sx[i] = __dadd_rn(raw, __dmul_rn(nz[i], log1p(exp(spread))));
-    } else {
-      sx[i] = raw;
+  uint64_t m = 0;
+  for (int e = 0; e < E; ++e)
+    if (h[e] >= kth) {
+      m |= 1ULL << e;
+      lists[static_cast<long long>(e) * T + atomicAdd(&counts[e], 1)] = t;
     }
-  }
-  for (int o = 16; o > 0; o >>= 1) cand |= __shfl_xor_sync(0xffffffffu, cand, o);
+  mask[t] = m;
+}
 
-  // exact top-k among candidates: max score, ties to the lowest index
-  uint64_t kept = 0;
-  for (int j = 0; j < k; ++j) {
-    double best = 0.0;
-    int bi = -1;
+struct PruneWsView {
+  const double* WT;
+  const int* lists;
+  const int* counts;
+  double* s_exact;
+  double* sp_exact;
+};
+
+// Exact fp64 logits for the candidates of expert blockIdx.y (matvec_row
+// order, separately rounded mul/add): thread = (candidate, projection), where
+// projection 0 is x.W_g and 1 (noisy) is x.W_noise. A warp shares one weight
+// row (broadcast loads); token rows stream in batches of 64 values so many
+// loads are in flight ahead of the dependent add chain.
+template <int DT>
+__device__ __forceinline__ void load8(const void* x, long long i, bool vec, double* o) {
+  if constexpr (DT == 2) {
+    if (vec) {
+      uint4 u = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(x) + i);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-    for (int i = 0; i < PS_PER; ++i) {
-      const int e = lane + 32 * i;
-      if (e < E && ((cand >> e) & 1ULL) && !((kept >> e) & 1ULL) && (bi < 0 || sx[i] > best)) {
-        best = sx[i];
-        bi = e;
+      for (int q = 0; q < 4; ++q) {
+        float2 f = __bfloat1622float2(h[q]);
+        o[2 * q] = f.x;
+        o[2 * q + 1] = f.y;
       }
+      return;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) {
-        best = ob;
-        bi = oi;
-      }
+  } else if constexpr (DT == 1) {
+    if (vec) {
+      float4 a = reinterpret_cast<const float4*>(static_cast<const float*>(x) + i)[0];
+      float4 b = reinterpret_cast<const float4*>(static_cast<const float*>(x) + i)[1];
+      o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+      return;
     }
-    kept |= 1ULL << bi;
   }
-
-  // saved tensors for the backward (exact where it matters, finite elsewhere)
 #pragma unroll
-  for (int i = 0; i < PS_PER; ++i) {
-    const int e = lane + 32 * i;
-    if (e >= E) continue;
+  for (int q = 0; q < 8; ++q) o[q] = load_as_double<DT>(x, i + q);
+}
+
+template <int DT, int NPROJ>
+__global__ void __launch_bounds__(128)
+    exact_kernel(const void* __restrict__ x, int T, int M, int E, const double* __restrict__ WT,
+                 const int* __restrict__ lists, const int* __restrict__ counts,
+                 double* __restrict__ raw_exact, double* __restrict__ sp_exact) {
+  const int e = blockIdx.y;
+  const int n = counts[e] * NPROJ;
+  const bool vec = (M % 8) == 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int proj = i % NPROJ;
+    const int t = lists[static_cast<long long>(e) * T + i / NPROJ];
+    const long long xrow = static_cast<long long>(t) * M;
+    const double* wr = WT + static_cast<long long>(proj * E + e) * M;
+    double acc = 0.0;
+    for (int j = 0; j < M; j += 8) {
+      double xv[8];
+      if (vec) load8<DT>(x, xrow + j, true, xv);
+      else
+        for (int q = 0; q < 8; ++q) xv[q] = j + q < M ? load_as_double<DT>(x, xrow + j + q) : 0.0;
+      const int jn = M - j < 8 ? M - j : 8;
+      for (int q = 0; q < jn; ++q) acc = __dadd_rn(acc, __dmul_rn(xv[q], wr[j + q]));
+    }
     const long long o = static_cast<long long>(t) * E + e;
-    if (scores_out) scores_out[o] = sx[i];
-    if (KIND == 0) {
-      if (noise_out) noise_out[o] = nz[i];
-      if (spread_out) spread_out[o] = spa[i];
-    }
+    if (proj == 0) raw_exact[o] = acc;
+    else sp_exact[o] = acc;
   }
+}
 
-  // weights over the kept set in ascending expert order (lane 0)
-  auto score_of = [&](int e) {
-    double v = 0.0;
-#pragma unroll
-    for (int i = 0; i < PS_PER; ++i) {
-      double s = __shfl_sync(0xffffffffu, sx[i], e & 31);
-      if ((e >> 5) == i) v = s;
-    }
-    return v;
+// Staged variant: a block takes EX_TOK candidates of one expert; their token
+// rows and the expert's weight rows stream through shared memory in EX_JC
+// chunks with TMA bulk copies (double-buffered, mbarrier completion), so the
+// dependent fp64 add chain of each thread reads operands at smem latency.
+// Thread = (candidate, projection).
+constexpr int EX_TOK = 64;
+
+template <int DT>
+struct Elem {
+  static constexpr int ES = DT == 0 ? 8 : DT == 1 ? 4 : 2;  // bytes per element
+  static constexpr int JC = DT == 0 ? 128 : 256;           // columns per stage
+  static constexpr int ROW = JC * ES + 16;                 // padded smem row stride
+};
+
+template <int DT, int NPROJ>
+__global__ void __launch_bounds__(EX_TOK * NPROJ)
+    exact_staged_kernel(const void* __restrict__ x, int T, int M, int E,
+                        const double* __restrict__ WT, const int* __restrict__ lists,
+                        const int* __restrict__ counts, double* __restrict__ raw_exact,
+                        double* __restrict__ sp_exact) {
+  constexpr int ES = Elem<DT>::ES, ROW = Elem<DT>::ROW, EX_JC = Elem<DT>::JC;
+  constexpr int XS_BYTES = EX_TOK * ROW;
+  constexpr int WS_BYTES = NPROJ * EX_JC * 8;
+  constexpr int STAGE = XS_BYTES + WS_BYTES;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ int toks[EX_TOK];
+  const int e = blockIdx.y;
+  const int c0 = blockIdx.x * EX_TOK;
+  const int n = counts[e];
+  if (c0 >= n) return;
+  const int nt = min(EX_TOK, n - c0);
+  const int tok = threadIdx.x % EX_TOK, proj = threadIdx.x / EX_TOK;
+  if (threadIdx.x < EX_TOK) toks[threadIdx.x] = threadIdx.x < nt ? lists[static_cast<long long>(e) * T + c0 + threadIdx.x] : 0;
+  if (threadIdx.x == 0) {
+    fsmoe_dev::mbar_init(&full[0], 1);
+    fsmoe_dev::mbar_init(&full[1], 1);
+    fsmoe_dev::fence_barrier_init();
+  }
+  __syncthreads();
+  const int nck = (M + EX_JC - 1) / EX_JC;
+  auto issue = [&](int ck) {
+    const int s = ck & 1;
+    uint8_t* st = smem + s * STAGE;
+    const int j0 = ck * EX_JC;
+    const int len = min(EX_JC, M - j0);
+    const uint32_t xb = static_cast<uint32_t>(len * ES), wb = static_cast<uint32_t>(len * 8);
+    fsmoe_dev::mbar_arrive_expect_tx(&full[s], xb * nt + wb * NPROJ);
+    for (int r = 0; r < nt; ++r)
+      fsmoe_dev::bulk_load(st + r * ROW,
+                           static_cast<const uint8_t*>(x) + (static_cast<long long>(toks[r]) * M + j0) * ES,
+                           xb, &full[s]);
+    for (int p = 0; p < NPROJ; ++p)
+      fsmoe_dev::bulk_load(st + XS_BYTES + p * EX_JC * 8, WT + static_cast<long long>(p * E + e) * M + j0,
+                           wb, &full[s]);
   };
-  const long long base = static_cast<long long>(t) * k;
-  if (KIND == 1) {
-    uint64_t m = kept;
+  if (threadIdx.x == 0) {
+    issue(0);
+    if (nck > 1) issue(1);
+  }
+  double acc = 0.0;
+  uint32_t ph[2] = {0, 0};
+  for (int ck = 0; ck < nck; ++ck) {
+    const int s = ck & 1;
+    fsmoe_dev::mbar_wait(&full[s], ph[s]);
+    ph[s] ^= 1;
+    const uint8_t* xr = smem + s * STAGE + tok * ROW;
+    const double* wr = reinterpret_cast<const double*>(smem + s * STAGE + XS_BYTES) + proj * EX_JC;
+    const int len = min(EX_JC, M - ck * EX_JC);
+    if (tok < nt) {
+      int j = 0;
+      for (; j + 8 <= len; j += 8) {
+        double xv[8];
+        load8<DT>(xr, j, true, xv);  // smem row, 16-byte aligned
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, __dmul_rn(xv[q], wr[j + q]));
+      }
+      for (; j < len; ++j) acc = __dadd_rn(acc, __dmul_rn(load_as_double<DT>(xr, j), wr[j]));
+    }
+    __syncthreads();  // stage s fully consumed
+    if (threadIdx.x == 0 && ck + 2 < nck) issue(ck + 2);
+  }
+  if (tok < nt) {
+    const long long o = static_cast<long long>(toks[tok]) * E + e;
+    if (proj == 0) raw_exact[o] = acc;
+    else sp_exact[o] = acc;
+  }
+}
+
+template <int DT, int NPROJ>
+void launch_exact(const void* x, int T, int M, int E, const PruneWsView& w, cudaStream_t st) {
+  // staged path needs 16-byte aligned row chunks: M * elem % 16 == 0
+  constexpr int ES = Elem<DT>::ES;
+  const bool staged = (static_cast<long long>(M) * ES) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  if (staged) {
+    constexpr int SMEM = 2 * (EX_TOK * Elem<DT>::ROW + NPROJ * Elem<DT>::JC * 8);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(exact_staged_kernel<DT, NPROJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      attr = true;
+    }
+    dim3 g((T + EX_TOK - 1) / EX_TOK, E);
+    exact_staged_kernel<DT, NPROJ><<<g, EX_TOK * NPROJ, SMEM, st>>>(x, T, M, E, w.WT, w.lists, w.counts,
+                                                                 w.s_exact, w.sp_exact);
+  } else {
+    dim3 eg((2 * T + 127) / 128 < 128 ? (2 * T + 127) / 128 : 128, E);
+    exact_kernel<DT, NPROJ><<<eg, 128, 0, st>>>(x, T, M, E, w.WT, w.lists, w.counts, w.s_exact,
+                                                w.sp_exact);
+  }
+  ::fsmoe::count_launch();
+}
+
+// Exact top-k among candidates, weights and picks (thread per token), then the
+// saved tensors for the backward written coalesced by the whole block.
+template <int KIND>
+__global__ void __launch_bounds__(128)
+    final_kernel(int T, int E, int k, const uint64_t* __restrict__ mask,
+                 double* __restrict__ s_exact, const double* __restrict__ sp_exact,
+                 const double* __restrict__ sapx, const double* __restrict__ spapx,
+                 const double* __restrict__ noise, int* __restrict__ pick_token,
+                 int* __restrict__ pick_expert, double* __restrict__ pick_weight,
+                 double* __restrict__ scores_out, double* __restrict__ noise_out,
+                 double* __restrict__ spread_out) {
+  const int t0 = blockIdx.x * blockDim.x;
+  const int t = t0 + threadIdx.x;
+  if (t < T) {
+    const uint64_t cand = mask[t];
+    const long long row = static_cast<long long>(t) * E;
+    if (KIND == 0)  // s = raw + n * softplus(spread)   (workload.cpp:186)
+      for (uint64_t m = cand; m; m &= m - 1) {
+        const long long o = row + __ffsll(static_cast<long long>(m)) - 1;
+        s_exact[o] = __dadd_rn(s_exact[o], __dmul_rn(noise[o], log1p(exp(sp_exact[o]))));
+      }
+    uint64_t kept = 0;
     for (int j = 0; j < k; ++j) {
-      const int e = __ffsll(static_cast<long long>(m)) - 1;
-      m &= m - 1;
-      const double s = score_of(e);
-      if (lane == 0) {
+      int bi = -1;
+      double best = 0.0;
+      for (uint64_t m = cand & ~kept; m; m &= m - 1) {
+        const int e = __ffsll(static_cast<long long>(m)) - 1;
+        const double s = s_exact[row + e];
+        if (bi < 0 || s > best) {
+          best = s;
+          bi = e;
+        }
+      }
+      kept |= 1ULL << bi;
+    }
+    const long long base = static_cast<long long>(t) * k;
+    if (KIND == 1) {
+      uint64_t m = kept;
+      for (int j = 0; j < k; ++j) {
+        const int e = __ffsll(static_cast<long long>(m)) - 1;
+        m &= m - 1;
         pick_token[base + j] = t;
         pick_expert[base + j] = e;
-        pick_weight[base + j] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-s)));
+        pick_weight[base + j] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-s_exact[row + e])));
+      }
+    } else {
+      uint64_t m = kept;
+      double mx = s_exact[row + __ffsll(static_cast<long long>(m)) - 1];
+      for (; m; m &= m - 1) {
+        const double s = s_exact[row + __ffsll(static_cast<long long>(m)) - 1];
+        mx = (mx < s) ? s : mx;
+      }
+      double z = 0.0;
+      for (m = kept; m; m &= m - 1)
+        z = __dadd_rn(z, exp(__dsub_rn(s_exact[row + __ffsll(static_cast<long long>(m)) - 1], mx)));
+      m = kept;
+      for (int j = 0; j < k; ++j) {
+        const int e = __ffsll(static_cast<long long>(m)) - 1;
+        m &= m - 1;
+        pick_token[base + j] = t;
+        pick_expert[base + j] = e;
+        pick_weight[base + j] = __ddiv_rn(exp(__dsub_rn(s_exact[row + e], mx)), z);
       }
     }
-    return;
   }
-  double ks[PS_MAXE];
-  int ke[PS_MAXE];
-  {
-    uint64_t m = kept;
-    for (int j = 0; j < k; ++j) {
-      const int e = __ffsll(static_cast<long long>(m)) - 1;
-      m &= m - 1;
-      ke[j] = e;
-      ks[j] = score_of(e);
+  // saved tensors: exact where a candidate (where gradients can be nonzero),
+  // the finite approximations elsewhere
+  const long long n = static_cast<long long>(min(T - t0, static_cast<int>(blockDim.x))) * E;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const long long o = static_cast<long long>(t0) * E + i;
+    const int tt = static_cast<int>(o / E), e = static_cast<int>(o % E);
+    const bool c = (mask[tt] >> e) & 1ULL;
+    if (scores_out) scores_out[o] = c ? s_exact[o] : sapx[o];
+    if (KIND == 0) {
+      if (noise_out) noise_out[o] = noise[o];
+      if (spread_out) spread_out[o] = c ? sp_exact[o] : spapx[o];
     }
   }
-  if (lane == 0) {
-    double mx = ks[0];
-    for (int j = 0; j < k; ++j) mx = (mx < ks[j]) ? ks[j] : mx;
-    double z = 0.0;
-    for (int j = 0; j < k; ++j) z = __dadd_rn(z, exp(__dsub_rn(ks[j], mx)));
-    for (int j = 0; j < k; ++j) {
-      pick_token[base + j] = t;
-      pick_expert[base + j] = ke[j];
-      pick_weight[base + j] = __ddiv_rn(exp(__dsub_rn(ks[j], mx)), z);
-    }
-  }
+}
+
+struct PruneWs {
+  float* W32;
+  double* WT;
+  double* wn;
+  float* part;
+  double* xn2;
+  uint64_t* draws;
+  double* noise;
+  double* sapx;
+  double* spapx;
+  double* lo;
+  double* hi;
+  uint64_t* mask;
+  int* lists;
+  int* counts;
+  double* s_exact;
+  double* sp_exact;
+  size_t bytes;
+};
+
+PruneWs carve(const fsmoe_gate_desc& d, void* base) {
+  const size_t T = d.tokens, E = d.score_cols, M = d.model_dim;
+  const size_t NC = d.kind == FSMOE_GATE_NOISY_TOPK ? 2 * E : E;
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* r = p ? p + off : nullptr;
+    off += (b + 255) & ~size_t(255);
+    return r;
+  };
+  PruneWs w;
+  w.W32 = reinterpret_cast<float*>(take(4 * M * NC));
+  w.WT = reinterpret_cast<double*>(take(8 * M * NC));
+  w.wn = reinterpret_cast<double*>(take(8 * NC));
+  w.part = reinterpret_cast<float*>(take(4 * AP_KS * T * NC));
+  w.xn2 = reinterpret_cast<double*>(take(8 * AP_KS * T));
+  w.draws = reinterpret_cast<uint64_t*>(take(8 * T * 2 * E));
+  w.noise = reinterpret_cast<double*>(take(8 * T * E));
+  w.sapx = reinterpret_cast<double*>(take(8 * T * E));
+  w.spapx = reinterpret_cast<double*>(take(8 * T * E));
+  w.lo = reinterpret_cast<double*>(take(8 * T * E));
+  w.hi = reinterpret_cast<double*>(take(8 * T * E));
+  w.mask = reinterpret_cast<uint64_t*>(take(8 * T));
+  w.lists = reinterpret_cast<int*>(take(4 * T * E));
+  w.counts = reinterpret_cast<int*>(take(4 * E));
+  w.s_exact = reinterpret_cast<double*>(take(8 * T * E));
+  w.sp_exact = reinterpret_cast<double*>(take(8 * T * E));
+  w.bytes = off;
+  return w;
 }
 
 }  // namespace
 
-size_t gate_prune_workspace_bytes(const fsmoe_gate_desc& d) {
-  const size_t T = d.tokens, E = d.score_cols, M = d.model_dim;
-  const size_t NC = d.kind == FSMOE_GATE_NOISY_TOPK ? 2 * E : E;
-  auto r = [](size_t b) { return (b + 255) & ~size_t(255); };
-  return r(4 * M * NC) + r(8 * NC) + r(4 * T * NC);
-}
+size_t gate_prune_workspace_bytes(const fsmoe_gate_desc& d) { return carve(d, nullptr).bytes; }
 
 bool gate_prune_applicable(const fsmoe_gate_desc& d) {
   if (d.kind != FSMOE_GATE_NOISY_TOPK && d.kind != FSMOE_GATE_SIGMOID_TOPK) return false;
-  if (d.score_cols > PS_MAXE || d.top_k > PS_MAXE) return false;
-  return true;
+  return d.score_cols <= PS_MAXE;
 }
 
 int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
@@ -362,47 +583,56 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
   const int T = d.tokens, M = d.model_dim, E = d.score_cols, k = d.top_k;
   const bool noisy = d.kind == FSMOE_GATE_NOISY_TOPK;
   const int NC = noisy ? 2 * E : E;
-  char* w = static_cast<char*>(ws);
-  auto take = [&](size_t bytes) {
-    char* p = w;
-    w += (bytes + 255) & ~size_t(255);
-    return p;
-  };
-  float* W32 = reinterpret_cast<float*>(take(4ull * M * NC));
-  double* wn = reinterpret_cast<double*>(take(8ull * NC));
-  float* approx = reinterpret_cast<float*>(take(4ull * T * NC));
-  w_to_f32_kernel<<<NC, 256, 0, st>>>(M, E, w_score, noisy ? E : 0, w_noise, W32, wn);
+  PruneWs w = carve(d, ws);
+  FSMOE_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int) * E, st), "gate memset");
+  w_prep_kernel<<<NC, 256, 0, st>>>(M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn);
   ::fsmoe::count_launch();
-  dim3 grid((T + AP_TOK - 1) / AP_TOK, (NC + AP_COL - 1) / AP_COL);
+  dim3 grid((T + AP_TOK - 1) / AP_TOK, (NC + AP_COL - 1) / AP_COL, AP_KS);
   switch (d.x_dtype) {
-    case FSMOE_F64: approx_scores_kernel<0><<<grid, 256, 0, st>>>(x, T, M, W32, NC, approx); break;
-    case FSMOE_F32: approx_scores_kernel<1><<<grid, 256, 0, st>>>(x, T, M, W32, NC, approx); break;
-    default: approx_scores_kernel<2><<<grid, 256, 0, st>>>(x, T, M, W32, NC, approx); break;
+    case FSMOE_F64: approx_scores_kernel<0><<<grid, 64, 0, st>>>(x, T, M, w.W32, NC, w.part, w.xn2); break;
+    case FSMOE_F32: approx_scores_kernel<1><<<grid, 64, 0, st>>>(x, T, M, w.W32, NC, w.part, w.xn2); break;
+    default: approx_scores_kernel<2><<<grid, 64, 0, st>>>(x, T, M, w.W32, NC, w.part, w.xn2); break;
   }
   ::fsmoe::count_launch();
-  // |s~ - s_ref| <= cB |x| |w|: fp32 rounding of x, w and the M-term FMA chain
-  // (+ slack), plus the reference's own fp64 sequential rounding.
-  const double cB = (M + 4.0) * 0x1.0p-24 * 1.01 + (M + 2.0) * 0x1.0p-53;
-  const int blocks = (T + 7) / 8;
-#define FSMOE_PS(DT, KIND)                                                                        \
-  prune_select_kernel<DT, KIND><<<blocks, 256, 0, st>>>(x, T, M, E, k, d.seed, approx, wn, cB,     \
-                                                        w_score, w_noise, pick_token, pick_expert, \
-                                                        pick_weight, scores_out, noise_out,        \
-                                                        spread_out)
   if (noisy) {
-    switch (d.x_dtype) {
-      case FSMOE_F64: FSMOE_PS(0, 0); break;
-      case FSMOE_F32: FSMOE_PS(1, 0); break;
-      default: FSMOE_PS(2, 0); break;
-    }
-  } else {
-    switch (d.x_dtype) {
-      case FSMOE_F64: FSMOE_PS(0, 1); break;
-      case FSMOE_F32: FSMOE_PS(1, 1); break;
-      default: FSMOE_PS(2, 1); break;
-    }
+    if (E <= 16) mt_kernel<16><<<(T + 127) / 128, 128, 0, st>>>(T, E, d.seed, w.draws);
+    else if (E <= 32) mt_kernel<32><<<(T + 127) / 128, 128, 0, st>>>(T, E, d.seed, w.draws);
+    else mt_kernel<64><<<(T + 127) / 128, 128, 0, st>>>(T, E, d.seed, w.draws);
+    ::fsmoe::count_launch();
   }
-#undef FSMOE_PS
+  // |s~ - s_ref| <= cB |x| |w|: fp32 rounding of x, w and the M-term FMA chain
+  // (+ the split partial sums, + 1% slack), plus the reference's own fp64
+  // sequential rounding.
+  const double cB = (M + AP_KS + 4.0) * 0x1.0p-24 * 1.01 + (M + 2.0) * 0x1.0p-53;
+  const long long pairs = static_cast<long long>(T) * E;
+  const int pb = static_cast<int>((pairs + 255) / 256);
+  if (noisy)
+    bound_kernel<0><<<pb, 256, 0, st>>>(T, E, M, w.part, w.xn2, w.wn, cB, w.draws, w.noise, w.sapx,
+                                        w.spapx, w.lo, w.hi);
+  else
+    bound_kernel<1><<<pb, 256, 0, st>>>(T, E, M, w.part, w.xn2, w.wn, cB, w.draws, w.noise, w.sapx,
+                                        w.spapx, w.lo, w.hi);
+  ::fsmoe::count_launch();
+  cand_kernel<<<(T + 127) / 128, 128, 0, st>>>(T, E, k, w.lo, w.hi, w.mask, w.lists, w.counts);
+  ::fsmoe::count_launch();
+  const PruneWsView v{w.WT, w.lists, w.counts, w.s_exact, w.sp_exact};
+  switch (d.x_dtype * 2 + (noisy ? 0 : 1)) {
+    case 0: launch_exact<0, 2>(x, T, M, E, v, st); break;
+    case 1: launch_exact<0, 1>(x, T, M, E, v, st); break;
+    case 2: launch_exact<1, 2>(x, T, M, E, v, st); break;
+    case 3: launch_exact<1, 1>(x, T, M, E, v, st); break;
+    case 4: launch_exact<2, 2>(x, T, M, E, v, st); break;
+    default: launch_exact<2, 1>(x, T, M, E, v, st); break;
+  }
+  const int tb = (T + 127) / 128;
+  if (noisy)
+    final_kernel<0><<<tb, 128, 0, st>>>(T, E, k, w.mask, w.s_exact, w.sp_exact, w.sapx, w.spapx,
+                                        w.noise, pick_token, pick_expert, pick_weight, scores_out,
+                                        noise_out, spread_out);
+  else
+    final_kernel<1><<<tb, 128, 0, st>>>(T, E, k, w.mask, w.s_exact, w.sp_exact, w.sapx, w.spapx,
+                                        w.noise, pick_token, pick_expert, pick_weight, scores_out,
+                                        noise_out, spread_out);
   ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_gate(prune)");
 }
