@@ -315,3 +315,13 @@ int orc_combine(int buf_rows, int buf_cols, const double* buffers, int T,
   }
   return 0;
 }
+
+/* FNV-1a 64 over n bytes (fingerprint helper for tests). */
+uint64_t orc_fnv1a64(const unsigned char* p, long long n) {
+  uint64_t h = 0xCBF29CE484222325ULL;
+  for (long long i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001B3ULL;
+  }
+  return h;
+}

@@ -76,6 +76,9 @@ int orc_combine(int buf_rows, int buf_cols, const double* buffers, int tokens,
                 long long n_slots_of_pick, const int* slot_of_pick, int model_dim,
                 double* y, char* err, int errlen);
 
+/* FNV-1a 64 over n bytes (test fingerprints). */
+uint64_t orc_fnv1a64(const unsigned char* p, long long n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -197,3 +197,85 @@ class MtRng:
 
     def matrix(self, rows: int, cols: int, lo: float, hi: float) -> np.ndarray:
         return self.uniform_array(rows * cols, lo, hi).reshape(rows, cols)
+
+
+# --------------------------------------------------------------- planner --
+
+class RefPlanner:
+    """The reference's control plane (cost_models / pipeline_optimizer /
+    schedule_sim / grad_partition), compiled from /root/reference by
+    oracle/Makefile, behind the same flat-array calls as include/fsmoe_plan.h."""
+
+    def __init__(self):
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(f"reference not built: {REF_SO} (make -C oracle ref)")
+        self.lib = C.CDLL(REF_SO)
+        self.lib.ref_capacity_tokens.restype = C.c_longlong
+
+    @staticmethod
+    def _d(a):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        return a, a.ctypes.data_as(C.POINTER(C.c_double))
+
+    @staticmethod
+    def _i(a):
+        a = np.ascontiguousarray(a, dtype=np.int32)
+        return a, a.ctypes.data_as(C.POINTER(C.c_int))
+
+    def _call(self, name, *args):
+        err = C.create_string_buffer(256)
+        rc = getattr(self.lib, name)(*args, err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+
+    def capacity_tokens(self, ints, dbls):
+        (ia, ip), (da, dp) = self._i(ints), self._d(dbls)
+        err = C.create_string_buffer(256)
+        v = self.lib.ref_capacity_tokens(ip, dp, err, 256)
+        if v < 0:
+            raise OracleError(2, err.value.decode())
+        return int(v)
+
+    def derive_volumes(self, ints, dbls, parallel):
+        (ia, ip), (da, dp), (pa, pp) = self._i(ints), self._d(dbls), self._i(parallel)
+        out, op = self._d(np.zeros(7))
+        self._call("ref_derive_volumes", ip, dp, pp, op)
+        return out
+
+    def fit_profile(self, kinds, ns, ts, min_r2):
+        (ka, kp), (na, np_), (ta, tp) = self._i(kinds), self._d(ns), self._d(ts)
+        prof, pp = self._d(np.zeros(10))
+        meta, mp = self._d(np.zeros(2))
+        self._call("ref_fit_profile", len(kinds), kp, np_, tp, C.c_double(min_r2), pp, mp)
+        return prof, meta[0], int(meta[1])
+
+    def find_degree(self, vol, prof, t_gar, mult, r_max):
+        (va, vp), (pa, pp) = self._d(vol), self._d(prof)
+        out, op = self._d(np.zeros(11))
+        self._call("ref_find_degree", vp, pp, C.c_double(t_gar), mult, r_max, op)
+        return out
+
+    def plan_layer(self, vol, prof, t_gar, r_max):
+        (va, vp), (pa, pp) = self._d(vol), self._d(prof)
+        out, op = self._d(np.zeros(10))
+        self._call("ref_plan_layer", vp, pp, C.c_double(t_gar), r_max, op)
+        return out
+
+    def build_partition_plan(self, layers_flat, n, prof, de, r_max):
+        (la, lp), (pa, pp), (da, dp) = self._d(layers_flat), self._d(prof), self._d(de)
+        out, op = self._d(np.zeros(9 * n + 4))
+        self._call("ref_build_partition_plan", n, lp, pp, dp, r_max, op)
+        return out
+
+    def simulate_stage(self, vol, prof, mult, r, sync, style):
+        (va, vp), (pa, pp), (sa, sp) = self._d(vol), self._d(prof), self._d(list(sync) or [0.0])
+        cap = 5 + 2 * (5 * r + len(sync) + 8)
+        out, op = self._d(np.zeros(cap))
+        self._call("ref_simulate_stage", vp, pp, mult, r, len(sync), sp, style, op, cap)
+        return out
+
+    def brute_force_degree(self, vol, prof, t_gar, mult, r_max):
+        (va, vp), (pa, pp) = self._d(vol), self._d(prof)
+        out, op = self._d(np.zeros(2))
+        self._call("ref_brute_force_degree", vp, pp, C.c_double(t_gar), mult, r_max, op)
+        return int(out[0]), out[1]

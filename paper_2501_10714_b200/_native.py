@@ -81,7 +81,9 @@ def check(rc: int, lib: C.CDLL | None = None) -> None:
     if rc == 0:
         return
     lib = lib or cuda_lib()
-    fn = lib.fsmoe_last_error if hasattr(lib, "fsmoe_last_error") else lib.fsmoe_layer_last_error
+    # libfsmoe.so keeps its own message slot (it also re-exports the CUDA
+    # library's symbols through its dependency, so test by identity).
+    fn = lib.fsmoe_layer_last_error if lib is _cpp else lib.fsmoe_last_error
     fn.restype = C.c_char_p
     msg = (fn() or b"").decode()
     if rc == 2:

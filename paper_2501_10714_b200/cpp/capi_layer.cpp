@@ -22,6 +22,14 @@ namespace {
 
 thread_local std::string g_err;
 
+}  // namespace
+
+namespace fsmoe {
+void set_layer_error(const std::string& msg) { g_err = msg; }
+}  // namespace fsmoe
+
+namespace {
+
 template <class F>
 int guard(F&& f) {
   try {

@@ -65,22 +65,26 @@ class MoEConfig:
         return int(math.ceil(v - 1e-9))
 
 
+def broadcast_unique_id(uid: bytes, world: int) -> bytes:
+    """Rank 0's 128-byte NCCL unique id to every rank (torch.distributed is
+    only the bootstrap channel; the data path is libfsmoe.so's own NCCL comm)."""
+    import torch.distributed as dist
+    if world <= 1 or not dist.is_initialized():
+        return uid
+    obj = [bytes(uid)]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
 class EpGroup:
-    """NCCL expert-parallel communicator owned by libfsmoe.so; torch.distributed
-    only broadcasts the 128-byte unique id."""
+    """NCCL expert-parallel communicator owned by libfsmoe.so."""
 
     def __init__(self, world: int, rank: int, device: int, max_ctas: int = 0):
-        import torch.distributed as dist
         lib = NL.cpp_lib()
         uid = (C.c_ubyte * 128)()
         if rank == 0:
             NL.check(lib.fsmoe_ep_unique_id(uid), lib)
-        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
-        if dist.is_initialized() and world > 1:
-            obj = [t]
-            dist.broadcast_object_list(obj, src=0)
-            t = obj[0]
-        uid = (C.c_ubyte * 128)(*t.tolist())
+        uid = (C.c_ubyte * 128)(*broadcast_unique_id(bytes(uid), world))
         h = C.c_void_p()
         NL.check(lib.fsmoe_ep_create(world, rank, uid, device, max_ctas, C.byref(h)), lib)
         self.h = h
