@@ -100,6 +100,30 @@ def _p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def gate_params(cfg: MoEConfig, init_seed: int):
+    """Replicated gate parameters (fp64, identical on every rank)."""
+    M, E = cfg.model_dim, cfg.experts
+    g = torch.Generator(device="cpu").manual_seed(init_seed)
+    rows = cfg.proj_dim if cfg.gate == "cosine_topk" else M
+    w_gate = (torch.rand(rows, E, generator=g, dtype=torch.float64) * 2 - 1) / math.sqrt(rows)
+    w_noise = (torch.rand(M, E, generator=g, dtype=torch.float64) * 2 - 1) / math.sqrt(M)
+    proj = None
+    if cfg.gate == "cosine_topk":
+        proj = (torch.rand(cfg.proj_dim, M, generator=g, dtype=torch.float64) * 2 - 1) / math.sqrt(M)
+    return w_gate, w_noise, proj
+
+
+def expert_params(cfg: MoEConfig, rank: int, world: int, init_seed: int):
+    """Rank-local expert weights [E_l][N1][M], [E_l][M][H] (fp32, CPU)."""
+    M, H = cfg.model_dim, cfg.ffn_dim
+    el = cfg.experts // world
+    n1 = 2 * H if cfg.ffn == "gated3" else H
+    ge = torch.Generator(device="cpu").manual_seed(init_seed * 1000 + 17 + rank)
+    w1 = (torch.rand(el, n1, M, generator=ge) * 2 - 1) / math.sqrt(M)
+    w2 = (torch.rand(el, M, H, generator=ge) * 2 - 1) / math.sqrt(H)
+    return w1, w2
+
+
 class MoELayer:
     """One FSMoE MoE layer on the current CUDA device (EP over `ep`)."""
 
@@ -115,19 +139,13 @@ class MoELayer:
         self.n1 = 2 * cfg.ffn_dim if cfg.ffn == "gated3" else cfg.ffn_dim
         self.act_dtype = torch.bfloat16 if cfg.precision == "bf16" else torch.float32
         M, H, E = cfg.model_dim, cfg.ffn_dim, cfg.experts
-        g = torch.Generator(device="cpu").manual_seed(init_seed)
-        rows = cfg.proj_dim if cfg.gate == "cosine_topk" else M
         # replicated gate parameters (same on every rank): fp64 master copies
-        self.w_gate = ((torch.rand(rows, E, generator=g, dtype=torch.float64) * 2 - 1) / math.sqrt(rows)).to(dev)
-        self.w_noise = ((torch.rand(M, E, generator=g, dtype=torch.float64) * 2 - 1) / math.sqrt(M)).to(dev)
-        self.proj = None
-        if cfg.gate == "cosine_topk":
-            self.proj = ((torch.rand(cfg.proj_dim, M, generator=g, dtype=torch.float64) * 2 - 1)
-                         / math.sqrt(M)).to(dev)
-        # rank-local experts (different stream per rank)
-        ge = torch.Generator(device="cpu").manual_seed(init_seed * 1000 + 17 + self.rank)
-        self.w1 = ((torch.rand(self.el, self.n1, M, generator=ge) * 2 - 1) / math.sqrt(M)).to(dev, self.act_dtype)
-        self.w2 = ((torch.rand(self.el, M, H, generator=ge) * 2 - 1) / math.sqrt(H)).to(dev, self.act_dtype)
+        wg, wn, pj = gate_params(cfg, init_seed)
+        self.w_gate, self.w_noise = wg.to(dev), wn.to(dev)
+        self.proj = pj.to(dev) if pj is not None else None
+        # rank-local experts (a different stream per rank)
+        w1, w2 = expert_params(cfg, self.rank, self.world, init_seed)
+        self.w1, self.w2 = w1.to(dev, self.act_dtype), w2.to(dev, self.act_dtype)
         self.g_gate = torch.zeros_like(self.w_gate)
         self.g_noise = torch.zeros_like(self.w_noise)
         self.g_proj = torch.zeros_like(self.proj) if self.proj is not None else None
@@ -177,6 +195,7 @@ class MoELayer:
             y = torch.empty_like(x)
         lib = NL.cpp_lib()
         NL.check(lib.fsmoe_layer_forward(self.h, _p(x), _p(y), self._stream()), lib)
+        self._x_saved = x  # the backward reads x (gate gradient): keep it alive
         return y
 
     def backward(self, dy, dx=None):

@@ -1,0 +1,123 @@
+"""Expert parallelism on real GPUs: the C++ executor (libfsmoe.so) with its
+own NCCL communicator over NVLink, world_size = min(4, visible GPUs) >= 2,
+pipeline degrees r_fwd != r_bwd. Every rank's outputs and gradients are
+compared with the fp64 restatement (oracle/layer_oracle.py) applied per rank
+with the union of experts; expert grads = sum of all ranks' contributions,
+gate grads allreduced. Skipped with fewer than 2 GPUs (run via
+`gpurun --gpus 2`)."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, precision, gate, ffn, rf, rb, q):
+    try:
+        sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+        import torch.distributed as dist
+
+        import layer_oracle
+        import pyoracle
+        from paper_2501_10714_b200.layer import (EpGroup, MoEConfig, MoELayer, expert_params,
+                                                 gate_params)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        T, M, H, E, k = 1024, 256, 256, 4 * world, 2
+        cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=k, gate=gate, ffn=ffn,
+                        precision=precision, seed=9, r_fwd=rf, r_bwd=rb, capacity=384)
+        ep = EpGroup(world, rank, rank)
+        layer = MoELayer(cfg, ep, init_seed=2)
+        dt = layer.act_dtype
+
+        def inputs(r):
+            g = torch.Generator().manual_seed(500 + r)
+            return (torch.rand(T, M, generator=g) * 2 - 1).to(dt), (torch.rand(T, M, generator=g) * 2 - 1).to(dt)
+
+        x, dy = inputs(rank)
+        y = layer.forward(x.cuda())
+        dx = layer.backward(dy.cuda())
+        torch.cuda.synchronize()
+
+        # union of experts (rank-major), rounded like the device copies
+        W1 = np.concatenate([expert_params(cfg, r, world, 2)[0].to(dt).double().numpy() for r in range(world)])
+        W2 = np.concatenate([expert_params(cfg, r, world, 2)[1].to(dt).double().numpy() for r in range(world)])
+        wg, wn, pj = (t.numpy() if t is not None else None for t in gate_params(cfg, 2))
+        orc = pyoracle.Oracle("port")
+        kk = layer.capacity if gate == "expert_choice" else k
+        sums = {}
+        mine = None
+        for r in range(world):
+            xr, dyr = inputs(r)
+            yr, cache = layer_oracle.forward(xr.double().numpy(), gate, kk, 9, layer.capacity, wg, wn, pj,
+                                             W1, W2, ffn, orc)
+            gr = layer_oracle.backward(cache, dyr.double().numpy(), gate, kk, layer.capacity, wg, wn, pj,
+                                       W1, W2, ffn)
+            for key in ("g_w1", "g_w2", "g_gate"):
+                sums[key] = sums.get(key, 0) + gr[key]
+            if r == rank:
+                mine = (yr, gr)
+        tol = 1e-4 if precision == "f32" else 3e-2
+
+        def rel(a, b):
+            a = a.double().cpu().numpy() if torch.is_tensor(a) else a
+            return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+        el = E // world
+        errs = {"y": rel(y, mine[0]), "dx": rel(dx, mine[1]["dx"]),
+                "g_w1": rel(layer.g_w1, sums["g_w1"][rank * el:(rank + 1) * el]),
+                "g_w2": rel(layer.g_w2, sums["g_w2"][rank * el:(rank + 1) * el])}
+        if np.abs(sums["g_gate"]).max() > 0:
+            errs["g_gate"] = rel(layer.g_gate, sums["g_gate"])
+            errs["g_gate_vs_local"] = rel(layer.g_gate, mine[1]["g_gate"])
+            errs["g_gate_vs_2sum"] = rel(layer.g_gate, 2 * sums["g_gate"])
+        bad = {a: b for a, b in errs.items() if not b < tol and "_vs_" not in a}
+        layer.close()
+        ep.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok" if not bad else f"bad {bad}", errs))
+    except Exception as e:
+        import traceback
+        q.put((rank, "error " + repr(e) + traceback.format_exc()[-2000:], {}))
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("precision,gate,ffn,rf,rb", [
+    ("f32", "noisy_topk", "simple", 1, 1),
+    ("f32", "sigmoid_topk", "gated3", 2, 3),
+    ("bf16", "noisy_topk", "simple", 3, 2),
+    ("bf16", "expert_choice", "gated3", 2, 1),
+])
+def test_ep_layer_matches_restatement(precision, gate, ffn, rf, rb):
+    import torch.multiprocessing as mp
+    world = min(4, torch.cuda.device_count())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, precision, gate, ffn, rf, rb, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        import json
+        with open(os.path.join(out, f"ep_{precision}_{gate}_{ffn}_{rf}{rb}.json"), "w") as f:
+            json.dump(res, f, indent=1, default=str)
+    assert all(s == "ok" for _, s, _ in res), res
