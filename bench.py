@@ -250,6 +250,33 @@ def gemm_roofline(layer, peaks, reps=5):
     }, flops, ms
 
 
+def timeline_summary(trace: str, steps: int):
+    """Per-phase device time (ms/step) from the layer's Chrome trace, plus how
+    much of the comm stream's time is NOT hidden under compute (exposed)."""
+    ev = json.loads(trace)["traceEvents"]
+    per = {}
+    comp, comm = [], []
+    for x in ev:
+        name = x["name"].split("[")[0]
+        per[name] = per.get(name, 0.0) + x["dur"] / 1e3
+        (comm if x["tid"] == 0 else comp).append((x["ts"], x["ts"] + x["dur"]))
+    comp.sort()
+    exposed = 0.0
+    for a, b in comm:
+        covered = 0.0
+        for c, d in comp:
+            lo, hi = max(a, c), min(b, d)
+            if hi > lo:
+                covered += hi - lo
+        exposed += (b - a) - covered
+    span = (max(b for _, b in comp + comm) - min(a for a, _ in comp + comm)) / 1e3
+    return {"phase_ms_per_step": {k: round(v / steps, 4) for k, v in sorted(per.items())},
+            "comm_ms_per_step": round(sum(b - a for a, b in comm) / 1e3 / steps, 4),
+            "comm_exposed_ms_per_step": round(exposed / 1e3 / steps, 4),
+            "traced_ms_per_step": round(span / steps, 4),
+            "note": "traced run synchronises per phase call; shares, not absolute step time"}
+
+
 def gpu_arm(args):
     import numpy as np
     import torch
@@ -344,6 +371,21 @@ def gpu_arm(args):
                "d2h_bytes_per_step": dx.numel() * dx.element_size(), "ms_per_step": ems,
                "api": "paper_2501_10714_b200.layer.MoELayer forward+backward (libfsmoe.so C ABI)"}
 
+    timeline = None
+    if args.trace:
+        nt = 3
+        layer.set_trace(True)
+        for _ in range(nt):
+            layer.forward(x, y)
+            layer.backward(dy, dx)
+        torch.cuda.synchronize()
+        tj = layer.trace_json()
+        layer.set_trace(False)
+        os.makedirs(os.path.dirname(os.path.abspath(args.trace)) or ".", exist_ok=True)
+        with open(f"{args.trace}.rank{rank}.json", "w") as f:
+            f.write(tj)
+        timeline = timeline_summary(tj, nt)
+
     roof, gflops, gms = gemm_roofline(layer, peaks)
     roof["peak_source"] = peak_kind
     traffic_file = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -382,6 +424,8 @@ def gpu_arm(args):
             "clocks": clk, "e2e": e2e, "gpu_launches": launches,
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu,
         }
+        if timeline:
+            line["timeline"] = timeline
         print(json.dumps(line), flush=True)
     layer.close()
     if ep:
@@ -402,6 +446,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace", default="", help="write per-rank measured timelines to PATH.rankN.json")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

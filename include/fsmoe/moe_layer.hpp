@@ -73,6 +73,10 @@ class MoELayer {
   // Named internal device buffers (for tests / inspection).
   void* buffer(const std::string& name, long long* bytes) const;
   long long dropped_host() const;  // synchronises
+  // Measured per-phase timeline (CUDA events on both streams; Chrome trace
+  // JSON with the schedule simulator's fields). Tracing synchronises each call.
+  void set_trace(bool on);
+  std::string trace_json() const;
 
  private:
   struct Impl;

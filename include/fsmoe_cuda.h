@@ -166,6 +166,46 @@ int fsmoe_gate_bwd(const fsmoe_gate_desc* d, const void* x, const double* w_scor
  * precision 0: bf16 operands on tcgen05 tensor cores (fp32 accumulate in
  * TMEM, TMA-fed); 1: fp32 SIMT check mode. See csrc/gemm.h for the two
  * problem shapes. */
+/* ---- peer memory (NVLink / NVSwitch) ------------------------------------
+ * The dispatch / combine AlltoAlls of the MoE layer are not separate
+ * collectives here: the kernel that produces a [P][E_l][C] block buffer
+ * (dispatch, combine backward, the expert GEMM epilogues) stores each row
+ * straight into the owning rank's buffer through CUDA-IPC-mapped peer
+ * pointers. A row of block b = p*E_l + e_l lands in base[p] at row
+ * (rank*E_l + e_l)*C + r%C (the receiver's layout is [P][E_l][C] by source
+ * rank). world = 1, rank = 0, base[0] = local buffer is the identity.
+ * Replaces the a2a tasks the reference only simulates (schedule_sim.cpp
+ * OpKind::a2a_dispatch / a2a_combine). */
+#define FSMOE_MAX_PEERS 8
+typedef struct fsmoe_peer_rows {
+  void* base[FSMOE_MAX_PEERS];
+  int world, rank, experts_local;
+  long long capacity;
+} fsmoe_peer_rows;
+
+/* Arrival flags: uint64 [nslots][world] in every rank's (IPC-shared) memory;
+ * signal adds 1 to flag[slot][rank] on every peer (release, system scope)
+ * after the stream's previous work, wait spins (acquire) until every
+ * flag[slot][src] >= target. Counters only grow: target = uses of the slot. */
+typedef struct fsmoe_peer_flags {
+  unsigned long long* base[FSMOE_MAX_PEERS];  /* per-rank flag arrays (base[rank] = local) */
+  int world, rank, nslots;
+} fsmoe_peer_flags;
+
+/* Optionally puts a small [P][E_l] row buffer (put_src, rows of put_row_bytes,
+ * mapped by put_dst with capacity 1) before raising the flag. */
+int fsmoe_peer_signal(const fsmoe_peer_flags* f, int slot, const void* put_src,
+                      long long put_row_bytes, const fsmoe_peer_rows* put_dst, void* stream);
+int fsmoe_peer_wait(const fsmoe_peer_flags* f, int slot, unsigned long long target, void* stream);
+/* fsmoe_dispatch / fsmoe_combine_bwd writing their block buffer through a peer map. */
+int fsmoe_dispatch_peer(int dtype, int model_dim, int experts, long long capacity,
+                        const int* pick_of_slot, const int* pick_token, const void* x,
+                        const fsmoe_peer_rows* dst, void* stream);
+int fsmoe_combine_bwd_peer(int dtype, int model_dim, int experts, long long capacity,
+                           long long n_picks, const int* pick_of_slot, const int* pick_token,
+                           const double* pick_weight, const void* dy, const void* buffers,
+                           const fsmoe_peer_rows* d_dst, double* d_weight, void* stream);
+
 typedef struct fsmoe_gemm_desc {
   int kind;        /* 0 row-grouped (fwd/dgrad), 1 k-grouped (wgrad) */
   int nblk, rows, K, N, Mo, No, n_w;
@@ -175,13 +215,19 @@ typedef struct fsmoe_gemm_desc {
   const void* A;
   const void* B;
   const long long* valid_rows; /* optional, per block */
-  int epi;         /* 0 store bf16, 1 store f32, 2 gelu fwd, 3 swiglu fwd, 4 gelu bwd, 5 swiglu bwd */
+  int epi;         /* 0 store bf16, 1 store f32, 2 gelu fwd, 3 swiglu fwd, 4 gelu bwd, 5 swiglu bwd.
+                    * bf16 gelu: fwd writes D = gelu'(Z) (what the backward
+                    * needs, so it does no transcendental work) and D2 = gelu(Z);
+                    * bwd writes D = acc * Zin with Zin that saved gelu'(Z). */
   void* D;
   void* D2;
   const void* Zin;
   long long ldd, ldd2, ldz;
   int accumulate;
   int precision;   /* 0 bf16/tcgen05, 1 fp32 check */
+  /* row-grouped epi 0/1 only: store output rows through this peer map
+   * ([nblk][rows_total] rows, capacity = rows_total) instead of D */
+  const fsmoe_peer_rows* d_peers;
 } fsmoe_gemm_desc;
 
 int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream);

@@ -68,6 +68,12 @@ int fsmoe_layer_bind(fsmoe_layer* layer, const fsmoe_layer_params* params);
 long long fsmoe_layer_capacity(const fsmoe_layer* layer);
 int fsmoe_layer_forward(fsmoe_layer* layer, const void* x, void* y, void* stream);
 int fsmoe_layer_backward(fsmoe_layer* layer, const void* dy, void* dx, void* stream);
+/* Measured timeline: enable per-phase CUDA-event tracing (synchronises each
+ * call); fsmoe_layer_trace copies the Chrome-trace JSON (fields and labels of
+ * the schedule simulator, tid 0 = comm stream, 2 = compute stream) and
+ * returns the bytes needed. */
+int fsmoe_layer_set_trace(fsmoe_layer* layer, int on);
+long long fsmoe_layer_trace(const fsmoe_layer* layer, char* buf, long long cap);
 /* Named internal device buffer (pick_token, slot_of_pick, fill, X_send, Z, ...). */
 int fsmoe_layer_buffer(const fsmoe_layer* layer, const char* name, void** ptr, long long* bytes);
 

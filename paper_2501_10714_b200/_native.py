@@ -43,6 +43,7 @@ class GemmDesc(C.Structure):
         ("valid_rows", C.c_void_p), ("epi", C.c_int), ("D", C.c_void_p), ("D2", C.c_void_p),
         ("Zin", C.c_void_p), ("ldd", C.c_longlong), ("ldd2", C.c_longlong),
         ("ldz", C.c_longlong), ("accumulate", C.c_int), ("precision", C.c_int),
+        ("d_peers", C.c_void_p),
     ]
 
 

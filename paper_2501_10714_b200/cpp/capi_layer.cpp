@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -144,6 +145,20 @@ int fsmoe_layer_forward(fsmoe_layer* layer, const void* x, void* y, void* stream
 
 int fsmoe_layer_backward(fsmoe_layer* layer, const void* dy, void* dx, void* stream) {
   return guard([&] { layer->l->backward(dy, dx, stream); });
+}
+
+int fsmoe_layer_set_trace(fsmoe_layer* layer, int on) {
+  return guard([&] { layer->l->set_trace(on != 0); });
+}
+
+long long fsmoe_layer_trace(const fsmoe_layer* layer, char* buf, long long cap) {
+  std::string j = layer->l->trace_json();
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>(j.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, j.data(), n);
+    buf[n] = '\0';
+  }
+  return static_cast<long long>(j.size()) + 1;
 }
 
 int fsmoe_layer_buffer(const fsmoe_layer* layer, const char* name, void** ptr, long long* bytes) {

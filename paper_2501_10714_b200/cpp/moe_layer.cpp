@@ -18,6 +18,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -59,8 +61,79 @@ std::vector<Chunk> make_chunks(long long C, int r) {
 
 }  // namespace
 
+// Measured timeline: CUDA events around every phase on the comm (lane 0 =
+// the simulator's inter_link) and compute (lane 2) streams, emitted as Chrome
+// trace events with the schedule simulator's fields and labels
+// (schedule_sim.cpp:351-367), so predicted and measured schedules diff.
+struct Tracer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Span {
+    std::string name;
+    int lane;
+    cudaEvent_t a, b;
+  };
+  std::vector<Span> spans;
+  cudaEvent_t base = nullptr;
+  std::string json;  // accumulated events
+  double offset_ms = 0.0;
+
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "event");
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void start(cudaStream_t s) {
+    if (!on) return;
+    base = next();
+    cuda_check(cudaEventRecord(base, s), "eventRecord");
+  }
+  int begin(const std::string& name, int lane, cudaStream_t s) {
+    if (!on) return -1;
+    cudaEvent_t e = next();
+    cuda_check(cudaEventRecord(e, s), "eventRecord");
+    spans.push_back({name, lane, e, nullptr});
+    return static_cast<int>(spans.size()) - 1;
+  }
+  void end(int i, cudaStream_t s) {
+    if (i < 0) return;
+    cudaEvent_t e = next();
+    cuda_check(cudaEventRecord(e, s), "eventRecord");
+    spans[static_cast<size_t>(i)].b = e;
+  }
+  void flush(const char* phase) {
+    if (!on || spans.empty()) return;
+    for (auto& sp : spans) cuda_check(cudaEventSynchronize(sp.b), "eventSync");
+    double call_end = 0.0;
+    char buf[256];
+    for (auto& sp : spans) {
+      float t0 = 0.f, t1 = 0.f;
+      cudaEventElapsedTime(&t0, base, sp.a);
+      cudaEventElapsedTime(&t1, base, sp.b);
+      std::snprintf(buf, sizeof buf,
+                    "%s{\"name\": \"%s.%s\", \"ph\": \"X\", \"ts\": %.3f, \"dur\": %.3f, "
+                    "\"pid\": 0, \"tid\": %d}",
+                    json.empty() ? "" : ",\n", phase, sp.name.c_str(), (offset_ms + t0) * 1000.0,
+                    (t1 - t0) * 1000.0, sp.lane);
+      json += buf;
+      call_end = std::max(call_end, static_cast<double>(t1));
+    }
+    offset_ms += call_end;
+    spans.clear();
+    used = 0;
+  }
+  ~Tracer() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 struct MoELayer::Impl {
   MoELayerConfig cfg;
+  Tracer tr;
   EpGroup* ep = nullptr;
   int P = 1, rank = 0, E = 0, El = 0, T = 0, M = 0, H = 0, N1 = 0, k = 0;
   long long C = 0, n_picks = 0;
@@ -91,6 +164,82 @@ struct MoELayer::Impl {
   void *Xs = nullptr, *Xr = nullptr, *Z = nullptr, *Hh = nullptr, *Or = nullptr, *Os = nullptr;
   void *dOs = nullptr, *dOr = nullptr, *dXr = nullptr, *dXs = nullptr;
 
+  // Peer-memory transport (default for P > 1; FSMOE_EP_TRANSPORT=nccl selects
+  // the grouped ncclSend/ncclRecv baseline). The four receive-side buffers,
+  // the received fills and the arrival flags live in one IPC-shared region;
+  // producers store rows straight into the owner's copy.
+  bool peer = false;
+  void* sym = nullptr;
+  std::vector<void*> sym_peers;
+  fsmoe_peer_rows map_X{}, map_O{}, map_dO{}, map_dX{}, map_fill{};
+  fsmoe_peer_flags flags{};
+  int n_chunk_slots = 1;
+  std::vector<unsigned long long> epoch;
+  bool last_was_bwd = false;
+  int slot_bar_fwd() const { return 0; }
+  int slot_disp_fwd() const { return 1; }
+  int slot_comb_fwd(size_t j) const { return 2 + static_cast<int>(j); }
+  int slot_disp_bwd() const { return 2 + n_chunk_slots; }
+  int slot_comb_bwd(size_t j) const { return 3 + n_chunk_slots + static_cast<int>(j); }
+  int slot_bar_bwd() const { return 3 + 2 * n_chunk_slots; }
+  int n_slots() const { return 4 + 2 * n_chunk_slots; }
+
+  void peer_signal(int slot, const void* put = nullptr, long long put_row_bytes = 0,
+                   const fsmoe_peer_rows* put_map = nullptr) {
+    throw_on(fsmoe_peer_signal(&flags, slot, put, put_row_bytes, put_map, s_comp));
+  }
+  void peer_wait(int slot) {
+    throw_on(fsmoe_peer_wait(&flags, slot, ++epoch[static_cast<size_t>(slot)], s_comp));
+  }
+
+  fsmoe_peer_rows make_map(size_t off, long long cap) const {
+    fsmoe_peer_rows m{};
+    m.world = P;
+    m.rank = rank;
+    m.experts_local = El;
+    m.capacity = cap;
+    for (int p = 0; p < P; ++p) m.base[p] = static_cast<char*>(sym_peers[p]) + off;
+    return m;
+  }
+
+  // [P][E_l][C] -> sym offsets; set up the maps and flags (collective).
+  void setup_peer(long long ab) {
+    auto al = [](size_t x) { return (x + 4095) & ~size_t(4095); };
+    size_t off = 0;
+    const size_t o_X = off; off = al(off + ab);
+    const size_t o_O = off; off = al(off + ab);
+    const size_t o_dO = off; off = al(off + ab);
+    const size_t o_dX = off; off = al(off + ab);
+    const size_t o_fill = off; off = al(off + 8 * static_cast<size_t>(E));
+    const size_t o_flags = off; off = al(off + 8 * static_cast<size_t>(n_slots()) * P);
+    cuda_check(cudaMalloc(&sym, off), "cudaMalloc");
+    // zero: padding rows are never written by the producers (flags start at 0)
+    cuda_check(cudaMemsetAsync(sym, 0, off, s_comp), "memset");
+    sym_peers = ep->map_peers(sym, s_comp);
+    char* b = static_cast<char*>(sym);
+    Xr = b + o_X;
+    Os = b + o_O;
+    dOr = b + o_dO;
+    dXs = b + o_dX;
+    rfill = reinterpret_cast<long long*>(b + o_fill);
+    alias("X_recv", Xr, ab);
+    alias("O_send", Os, ab);
+    alias("dO_recv", dOr, ab);
+    alias("dX_send", dXs, ab);
+    alias("recv_fill", rfill, 8LL * E);
+    map_X = make_map(o_X, C);
+    map_O = make_map(o_O, C);
+    map_dO = make_map(o_dO, C);
+    map_dX = make_map(o_dX, C);
+    map_fill = make_map(o_fill, 1);
+    flags.world = P;
+    flags.rank = rank;
+    flags.nslots = n_slots();
+    for (int p = 0; p < P; ++p)
+      flags.base[p] = reinterpret_cast<unsigned long long*>(static_cast<char*>(sym_peers[p]) + o_flags);
+    epoch.assign(static_cast<size_t>(n_slots()), 0);
+  }
+
   void* dalloc(const std::string& name, long long bytes) {
     void* p = nullptr;
     cuda_check(cudaMalloc(&p, static_cast<size_t>(std::max<long long>(bytes, 16))), "cudaMalloc");
@@ -103,6 +252,8 @@ struct MoELayer::Impl {
   ~Impl() {
     if (s_comp) cudaStreamSynchronize(s_comp);
     if (s_comm) cudaStreamSynchronize(s_comm);
+    if (ep && !sym_peers.empty()) ep->unmap_peers(sym_peers);
+    if (sym) cudaFree(sym);
     for (void* p : owned) cudaFree(p);
     for (auto e : ev_a) cudaEventDestroy(e);
     for (auto e : ev_b) cudaEventDestroy(e);
@@ -170,6 +321,7 @@ struct MoELayer::Impl {
     g2.D = Or;
     g2.ldd = M;
     g2.epi = bf ? 0 : 1;
+    if (peer) g2.d_peers = &map_O;  // combine AlltoAll fused into the epilogue
     gemm(g2);
   }
 
@@ -227,6 +379,7 @@ struct MoELayer::Impl {
     d1.D = dXr;
     d1.ldd = M;
     d1.epi = bf ? 0 : 1;
+    if (peer) d1.d_peers = &map_dX;  // backward combine fused into the epilogue
     gemm(d1);
   }
 
@@ -370,7 +523,11 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   I.status = static_cast<int*>(I.dalloc("status", 8));
   I.fill = static_cast<long long*>(I.dalloc("fill", 8 * E));
   I.dropped = static_cast<long long*>(I.dalloc("dropped", 8));
-  I.rfill = I.P > 1 ? static_cast<long long*>(I.dalloc("recv_fill", 8 * E)) : I.fill;
+  if (I.P > 1) {
+    const char* tr = std::getenv("FSMOE_EP_TRANSPORT");
+    I.peer = !(tr && std::strcmp(tr, "nccl") == 0);
+  }
+  I.rfill = I.P > 1 && !I.peer ? static_cast<long long*>(I.dalloc("recv_fill", 8 * E)) : I.fill;
   I.scores = static_cast<double*>(I.dalloc("scores", 8 * T * E));
   if (cfg.gate == GateKind::noisy_topk) {
     I.noise = static_cast<double*>(I.dalloc("noise", 8 * T * E));
@@ -388,6 +545,15 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
 
   const long long rows = E * C;  // == P * E_l * C on both sides
   const long long ab = rows * M * I.esz;
+  if (I.peer) {
+    I.n_chunk_slots = static_cast<int>(std::max(I.fwd_chunks.size(), I.bwd_chunks.size()));
+    I.setup_peer(ab);
+    I.Z = I.dalloc("Z", rows * I.N1 * I.esz);
+    I.Hh = I.dalloc("H", rows * I.H * I.esz);
+    cuda_check(cudaMemsetAsync(I.status, 0, 8, I.s_comp), "memset");
+    cuda_check(cudaStreamSynchronize(I.s_comp), "sync");
+    return;
+  }
   I.Xs = I.dalloc("X_send", ab);
   I.Xr = I.P > 1 ? I.dalloc("X_recv", ab) : I.Xs;
   if (I.P == 1) I.alias("X_recv", I.Xr, ab);
@@ -422,45 +588,84 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   I.record(I.ev_in, st);
   I.wait(I.s_comp, I.ev_in);
+  I.tr.start(I.s_comp);
   I.x_last = x;
+  // every earlier use of this layer's receive buffers is finished here; the
+  // wait for the peers' matching signal hides behind the gate
+  if (I.peer) I.peer_signal(I.slot_bar_fwd());
   // K1 gate, K2 assign, token index, K3 dispatch
+  int sp = I.tr.begin("gate", 2, I.s_comp);
   throw_on(fsmoe_gate(&I.gd, x, I.prm.w_gate, I.prm.w_noise, I.prm.proj, I.tok, I.exp, I.w,
                       I.scores, I.noise, I.spread, I.proj_out, I.status, I.gate_ws, I.gate_wsb,
                       I.s_comp));
+  I.tr.end(sp, I.s_comp);
+  sp = I.tr.begin("order", 2, I.s_comp);
   throw_on(fsmoe_assign(I.n_picks, I.tok, I.exp, I.T, I.E, I.C, I.slot, I.fill, I.dropped, I.pos,
                         I.status, I.assign_ws, I.assign_wsb, I.s_comp));
   const int kmajor = cfg_.gate == GateKind::expert_choice ? 0 : I.k;
   throw_on(fsmoe_token_index(I.n_picks, I.tok, I.T, kmajor, I.tptr, I.tpick, I.tidx_ws,
                              I.tidx_wsb, I.s_comp));
-  throw_on(fsmoe_dispatch(I.dtype, I.M, I.E, I.C, 1, I.pos, I.tok, x, I.Xs, I.s_comp));
+  if (!I.peer)
+    throw_on(fsmoe_dispatch(I.dtype, I.M, I.E, I.C, 1, I.pos, I.tok, x, I.Xs, I.s_comp));
+  I.tr.end(sp, I.s_comp);
   const auto& ch = I.fwd_chunks;
-  if (I.P > 1) {
-    I.record(I.ev_gate, I.s_comp);
-    I.wait(I.s_comm, I.ev_gate);
-    I.exchange_fill();
+  if (I.peer) {
+    // order + dispatch AlltoAll in one kernel: rows go straight to their owner
+    sp = I.tr.begin("dispatch", 0, I.s_comp);
+    I.peer_wait(I.slot_bar_fwd());
+    throw_on(fsmoe_dispatch_peer(I.dtype, I.M, I.E, I.C, I.pos, I.tok, x, &I.map_X, I.s_comp));
+    I.peer_signal(I.slot_disp_fwd(), I.fill, 8, &I.map_fill);
+    I.peer_wait(I.slot_disp_fwd());
+    I.tr.end(sp, I.s_comp);
     for (size_t i = 0; i < ch.size(); ++i) {
-      I.exchange(I.Xs, I.Xr, ch[i]);
-      I.record(I.ev_a[i], I.s_comm);
+      // GEMM2's epilogue stores the combine AlltoAll into the owners' O_send
+      sp = I.tr.begin("expert[" + std::to_string(i) + "]", 2, I.s_comp);
+      I.expert_fwd(ch[i]);
+      I.peer_signal(I.slot_comb_fwd(i));
+      I.tr.end(sp, I.s_comp);
     }
-  }
-  for (size_t i = 0; i < ch.size(); ++i) {
-    if (I.P > 1) I.wait(I.s_comp, I.ev_a[i]);
-    I.expert_fwd(ch[i]);
-    if (I.P > 1) I.record(I.ev_b[i], I.s_comp);
-  }
-  if (I.P > 1) {
+    sp = I.tr.begin("combine", 0, I.s_comp);
+    for (size_t i = 0; i < ch.size(); ++i) I.peer_wait(I.slot_comb_fwd(i));
+    I.tr.end(sp, I.s_comp);
+  } else {
+    if (I.P > 1) {
+      I.record(I.ev_gate, I.s_comp);
+      I.wait(I.s_comm, I.ev_gate);
+      I.exchange_fill();
+      for (size_t i = 0; i < ch.size(); ++i) {
+        sp = I.tr.begin("dispatch[" + std::to_string(i) + "]", 0, I.s_comm);
+        I.exchange(I.Xs, I.Xr, ch[i]);
+        I.tr.end(sp, I.s_comm);
+        I.record(I.ev_a[i], I.s_comm);
+      }
+    }
     for (size_t i = 0; i < ch.size(); ++i) {
-      I.wait(I.s_comm, I.ev_b[i]);
-      I.exchange(I.Or, I.Os, ch[i]);
+      if (I.P > 1) I.wait(I.s_comp, I.ev_a[i]);
+      sp = I.tr.begin("expert[" + std::to_string(i) + "]", 2, I.s_comp);
+      I.expert_fwd(ch[i]);
+      I.tr.end(sp, I.s_comp);
+      if (I.P > 1) I.record(I.ev_b[i], I.s_comp);
     }
-    I.record(I.ev_join, I.s_comm);
-    I.wait(I.s_comp, I.ev_join);
+    if (I.P > 1) {
+      for (size_t i = 0; i < ch.size(); ++i) {
+        I.wait(I.s_comm, I.ev_b[i]);
+        sp = I.tr.begin("combine[" + std::to_string(i) + "]", 0, I.s_comm);
+        I.exchange(I.Or, I.Os, ch[i]);
+        I.tr.end(sp, I.s_comm);
+      }
+      I.record(I.ev_join, I.s_comm);
+      I.wait(I.s_comp, I.ev_join);
+    }
   }
   // K5 combine
+  sp = I.tr.begin("i-order", 2, I.s_comp);
   throw_on(fsmoe_combine(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.w, I.Os, y,
                          I.s_comp));
+  I.tr.end(sp, I.s_comp);
+  I.last_was_bwd = false;
   I.record(I.ev_out, I.s_comp);
   I.wait(st, I.ev_out);
+  I.tr.flush("fwd");
 }
 
 void MoELayer::backward(const void* dy, void* dx, void* stream) {
@@ -469,6 +674,7 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   I.record(I.ev_in, st);
   I.wait(I.s_comp, I.ev_in);
+  I.tr.start(I.s_comp);
   const MoEParams& p = I.prm;
   // gate gradients accumulate inside gate_bwd: start from zero
   const long long ge = static_cast<long long>(I.gd.score_rows) * I.E;
@@ -476,44 +682,101 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
   if (p.g_noise) cuda_check(cudaMemsetAsync(p.g_noise, 0, 8LL * I.M * I.E, I.s_comp), "memset");
   if (p.g_proj)
     cuda_check(cudaMemsetAsync(p.g_proj, 0, 8LL * cfg_.proj_dim * I.M, I.s_comp), "memset");
+  const auto& ch = I.bwd_chunks;
+  int sp = -1;
+  if (I.peer) {
+    // a backward directly after a backward: the peers' previous reads of
+    // dO_recv / dX_send must be finished (after a forward its barrier did it)
+    if (I.last_was_bwd) {
+      I.peer_signal(I.slot_bar_bwd());
+      I.peer_wait(I.slot_bar_bwd());
+    }
+    // I-order backward fused with the dispatch AlltoAll of dO
+    sp = I.tr.begin("i-order", 2, I.s_comp);
+    throw_on(fsmoe_combine_bwd_peer(I.dtype, I.M, I.E, I.C, I.n_picks, I.pos, I.tok, I.w, dy, I.Os,
+                                    &I.map_dO, I.dw, I.s_comp));
+    I.tr.end(sp, I.s_comp);
+    sp = I.tr.begin("dispatch", 0, I.s_comp);
+    I.peer_signal(I.slot_disp_bwd());
+    I.peer_wait(I.slot_disp_bwd());
+    I.tr.end(sp, I.s_comp);
+    if (I.prm.dense_grad && cfg_.dense_grad_elems > 0) {
+      // gradient allreduce slices on the comm stream, overlapping expert backward
+      I.record(I.ev_gate, I.s_comp);
+      I.wait(I.s_comm, I.ev_gate);
+      sp = I.tr.begin("grad_sync", 0, I.s_comm);
+      I.allreduce_slices();
+      I.tr.end(sp, I.s_comm);
+      I.record(I.ev_join, I.s_comm);
+    }
+    for (size_t j = 0; j < ch.size(); ++j) {
+      // dgrad1's epilogue stores the combine AlltoAll into the owners' dX_send
+      sp = I.tr.begin("expert[" + std::to_string(j) + "]", 2, I.s_comp);
+      I.expert_bwd(ch[j], j == 0);
+      I.peer_signal(I.slot_comb_bwd(j));
+      I.tr.end(sp, I.s_comp);
+    }
+    sp = I.tr.begin("combine", 0, I.s_comp);
+    for (size_t j = 0; j < ch.size(); ++j) I.peer_wait(I.slot_comb_bwd(j));
+    I.tr.end(sp, I.s_comp);
+    if (I.prm.dense_grad && cfg_.dense_grad_elems > 0) I.wait(I.s_comp, I.ev_join);
+  } else {
   // I-order backward: dO (send side) and d weights
+  sp = I.tr.begin("i-order", 2, I.s_comp);
   throw_on(fsmoe_combine_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.n_picks, I.pos, I.tok, I.w, I.slot,
                              dy, I.Os, I.dOs, I.dw, I.s_comp));
-  const auto& ch = I.bwd_chunks;
+  I.tr.end(sp, I.s_comp);
   if (I.P > 1) {
     I.record(I.ev_gate, I.s_comp);
     I.wait(I.s_comm, I.ev_gate);
     for (size_t j = 0; j < ch.size(); ++j) {
+      sp = I.tr.begin("dispatch[" + std::to_string(j) + "]", 0, I.s_comm);
       I.exchange(I.dOs, I.dOr, ch[j]);
+      I.tr.end(sp, I.s_comm);
       I.record(I.ev_a[j], I.s_comm);
     }
     // gradient allreduce slices between the last dispatch and the first combine
+    sp = I.tr.begin("grad_sync", 0, I.s_comm);
     I.allreduce_slices();
+    I.tr.end(sp, I.s_comm);
   }
   for (size_t j = 0; j < ch.size(); ++j) {
     if (I.P > 1) I.wait(I.s_comp, I.ev_a[j]);
+    sp = I.tr.begin("expert[" + std::to_string(j) + "]", 2, I.s_comp);
     I.expert_bwd(ch[j], j == 0);
+    I.tr.end(sp, I.s_comp);
     if (I.P > 1) I.record(I.ev_b[j], I.s_comp);
   }
   if (I.P > 1) {
     for (size_t j = 0; j < ch.size(); ++j) {
       I.wait(I.s_comm, I.ev_b[j]);
+      sp = I.tr.begin("combine[" + std::to_string(j) + "]", 0, I.s_comm);
       I.exchange(I.dXr, I.dXs, ch[j]);
+      I.tr.end(sp, I.s_comm);
     }
     I.record(I.ev_join, I.s_comm);
     I.wait(I.s_comp, I.ev_join);
   }
+  }
   // Order backward, then the gate's contribution to dx and its parameters
+  sp = I.tr.begin("order", 2, I.s_comp);
   throw_on(fsmoe_dispatch_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.dXs, dx,
                               0, I.s_comp));
+  I.tr.end(sp, I.s_comp);
   if (!I.x_last) throw ConfigError("layer: backward before forward");
+  sp = I.tr.begin("gate", 2, I.s_comp);
   throw_on(fsmoe_gate_bwd(&I.gd, I.x_last, p.w_gate, p.w_noise, p.proj,
                           I.tok, I.exp, I.w, I.dw, I.scores, I.noise, I.spread, I.proj_out, dx,
                           p.g_gate, p.g_noise, p.g_proj, I.gbwd_ws, I.gbwd_wsb, I.s_comp));
-  if (I.P > 1) {
+  I.tr.end(sp, I.s_comp);
+  // A softmax over one survivor has a constant weight: the gate gradient is
+  // exactly zero on every rank (gate_bwd.cu), so there is nothing to reduce.
+  const bool gate_grad_zero = I.gd.top_k == 1 && cfg_.gate != GateKind::sigmoid_topk;
+  if (I.P > 1 && !gate_grad_zero) {
     // replicated gate parameters: sum their gradients over the EP group
     I.record(I.ev_gate, I.s_comp);
     I.wait(I.s_comm, I.ev_gate);
+    sp = I.tr.begin("gate_grad_sync", 0, I.s_comm);
     nccl_check(ncclGroupStart(), "ncclGroupStart");
     nccl_check(ncclAllReduce(p.g_gate, p.g_gate, ge, ncclFloat64, ncclSum, I.ep->comm(), I.s_comm),
                "ncclAllReduce");
@@ -526,11 +789,24 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
                                ncclFloat64, ncclSum, I.ep->comm(), I.s_comm),
                  "ncclAllReduce");
     nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    I.tr.end(sp, I.s_comm);
     I.record(I.ev_join, I.s_comm);
     I.wait(I.s_comp, I.ev_join);
   }
+  I.last_was_bwd = true;
   I.record(I.ev_out, I.s_comp);
   I.wait(st, I.ev_out);
+  I.tr.flush("bwd");
+}
+
+void MoELayer::set_trace(bool on) {
+  impl_->tr.on = on;
+  impl_->tr.json.clear();
+  impl_->tr.offset_ms = 0.0;
+}
+
+std::string MoELayer::trace_json() const {
+  return "{\"displayTimeUnit\": \"ms\", \"traceEvents\": [\n" + impl_->tr.json + "\n]}\n";
 }
 
 void* MoELayer::buffer(const std::string& name, long long* bytes) const {

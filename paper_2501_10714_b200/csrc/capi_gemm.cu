@@ -5,6 +5,7 @@
 
 #include "capi_common.h"
 #include "gemm.h"
+#include "kernels.h"
 
 namespace fsmoe {
 
@@ -132,6 +133,16 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   p.ldz = d->ldz;
   p.accumulate = d->accumulate != 0;
   if (d->epi < 0 || d->epi > 5) return config_error("gemm: unknown epilogue");
+  if (d->d_peers) {
+    const fsmoe_peer_rows* m = d->d_peers;
+    if (d->kind != 0 || d->epi > 1)
+      return config_error("gemm: peer output needs a row-grouped plain-store epilogue");
+    if (m->world < 1 || m->world > FSMOE_MAX_PEERS || m->rank < 0 || m->rank >= m->world ||
+        m->experts_local * m->world != d->nblk || m->capacity != (d->rows_total > 0 ? d->rows_total : d->rows))
+      return config_error("gemm: peer map does not match nblk / rows_total");
+    p.use_peers = true;
+    p.peers = peer_rows_of(m);
+  }
   if (p.kind == GemmKind::KGrouped && p.epi != Epi::StoreF32)
     return config_error("gemm: k-grouped (wgrad) problems take the f32 store epilogue");
   int rc = d->precision == 1 ? gemm_simt_launch(p, as_stream(stream))

@@ -142,7 +142,39 @@ int fsmoe_dispatch(int dtype, int model_dim, int experts, long long capacity, in
   if (capacity <= 0) return config_error("dispatch: capacity must be positive");
   if (chunks < 1 || chunks > capacity) return config_error("dispatch: chunks must be in [1, capacity]");
   return dispatch_launch(dtype, model_dim, experts, capacity, chunks, pick_of_slot, pick_token, x,
-                         buffers, as_stream(stream));
+                         local_rows(buffers), as_stream(stream));
+}
+
+static int check_peer_map(const fsmoe_peer_rows* m, int experts, long long capacity) {
+  if (!m) return config_error("peer map: null");
+  if (m->world < 1 || m->world > FSMOE_MAX_PEERS || m->rank < 0 || m->rank >= m->world)
+    return config_error("peer map: world must be in [1, 8] and rank in [0, world)");
+  if (m->experts_local * m->world != experts || m->capacity != capacity)
+    return config_error("peer map: experts_local * world must equal experts and capacity match");
+  for (int p = 0; p < m->world; ++p)
+    if (!m->base[p]) return config_error("peer map: missing peer buffer");
+  return FSMOE_OK;
+}
+
+int fsmoe_dispatch_peer(int dtype, int model_dim, int experts, long long capacity,
+                        const int* pick_of_slot, const int* pick_token, const void* x,
+                        const fsmoe_peer_rows* dst, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (capacity <= 0) return config_error("dispatch: capacity must be positive");
+  if (int rc = check_peer_map(dst, experts, capacity)) return rc;
+  return dispatch_launch(dtype, model_dim, experts, capacity, 1, pick_of_slot, pick_token, x,
+                         peer_rows_of(dst), as_stream(stream));
+}
+
+int fsmoe_combine_bwd_peer(int dtype, int model_dim, int experts, long long capacity,
+                           long long n_picks, const int* pick_of_slot, const int* pick_token,
+                           const double* pick_weight, const void* dy, const void* buffers,
+                           const fsmoe_peer_rows* d_dst, double* d_weight, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (int rc = check_peer_map(d_dst, experts, capacity)) return rc;
+  return combine_bwd_launch(dtype, model_dim, experts, capacity, 1, n_picks, pick_of_slot,
+                            pick_token, pick_weight, dy, buffers, peer_rows_of(d_dst), d_weight,
+                            as_stream(stream));
 }
 
 int fsmoe_combine(int dtype, int tokens, int model_dim, int experts, long long capacity,
@@ -164,7 +196,7 @@ int fsmoe_combine_bwd(int dtype, int tokens, int model_dim, int experts, long lo
   (void)slot_of_pick;
   if (int rc = check_dtype(dtype)) return rc;
   return combine_bwd_launch(dtype, model_dim, experts, capacity, chunks, n_picks, pick_of_slot,
-                            pick_token, pick_weight, dy, buffers, d_buffers, d_weight,
+                            pick_token, pick_weight, dy, buffers, local_rows(d_buffers), d_weight,
                             as_stream(stream));
 }
 

@@ -29,6 +29,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "route_common.cuh"
+
 namespace fsmoe {
 
 enum class GemmKind : int { RowGrouped = 0, KGrouped = 1 };
@@ -36,9 +38,9 @@ enum class GemmKind : int { RowGrouped = 0, KGrouped = 1 };
 enum class Epi : int {
   StoreBF16 = 0,   // D bf16
   StoreF32 = 1,    // D fp32 (accumulate when `accumulate`)
-  GeluFwd = 2,     // Z = acc (bf16), H = gelu(acc) (bf16)           N = H
+  GeluFwd = 2,     // D = gelu'(acc) (bf16, what the backward needs), D2 = H = gelu(acc)
   SwigluFwd = 3,   // acc cols interleaved [gate128|up128]: Z = acc, H = silu(g)*u
-  GeluBwd = 4,     // acc = dH; dZ = dH * gelu'(Z)                   N = H
+  GeluBwd = 4,     // acc = dH; dZ = dH * Zin, Zin = the saved gelu'(Z)  N = H
   SwigluBwd = 5,   // acc = dH (N = H); writes dZ at interleaved gate/up columns
 };
 
@@ -65,6 +67,10 @@ struct GemmProblem {
   long long ldd2 = 0;        // D2 row stride
   long long ldz = 0;         // Zin row stride
   bool accumulate = false;   // StoreF32: D += acc
+  // Row-grouped StoreBF16 / StoreF32: output row r of [nblk][rows_total] goes
+  // through this peer map (NVLink stores into the owning rank) instead of D.
+  bool use_peers = false;
+  fsmoe_dev::PeerRows peers{};
 };
 
 // bf16 operands, fp32 accumulate in TMEM (tcgen05). Returns cudaError_t.

@@ -19,6 +19,8 @@ struct SParams {
   float* D;
   long long ldd;
   int accumulate;
+  int use_peers;
+  fsmoe_dev::PeerRows peers;
 };
 
 __device__ __forceinline__ int valid_rows(const SParams& p, int b) {
@@ -102,7 +104,10 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SParams p) {
     for (int j = 0; j < 4; ++j) {
       int c = n0 + tx * 4 + j;
       if (c >= out_cols) continue;
-      float* d = p.D + (p.kind == 0 ? (static_cast<long long>(g) * p.rows_total + p.row0 + r) : (static_cast<long long>(g) * p.Mo + r)) * p.ldd + c;
+      const long long orow = p.kind == 0 ? static_cast<long long>(g) * p.rows_total + p.row0 + r
+                                         : static_cast<long long>(g) * p.Mo + r;
+      float* d = (p.use_peers ? reinterpret_cast<float*>(fsmoe_dev::peer_row(p.peers, orow, p.ldd * 4))
+                              : p.D + orow * p.ldd) + c;
       *d = p.accumulate ? *d + acc[i][j] : acc[i][j];
     }
   }
@@ -132,6 +137,8 @@ int gemm_simt_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.D = static_cast<float*>(pr.D);
   p.ldd = pr.ldd;
   p.accumulate = pr.accumulate ? 1 : 0;
+  p.use_peers = pr.use_peers ? 1 : 0;
+  p.peers = pr.peers;
   dim3 grid;
   if (pr.kind == GemmKind::RowGrouped) {
     grid = dim3((pr.N + TN - 1) / TN, (pr.rows + TM - 1) / TM, pr.nblk);

@@ -49,6 +49,8 @@ struct KParams {
   int rows_total, row0;  // block row window (see gemm.h)
   int accumulate;
   int out_rows, out_cols;  // valid output extent per group
+  int use_peers;           // row-grouped plain stores through `peers`
+  fsmoe_dev::PeerRows peers;
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -92,13 +94,25 @@ __device__ __forceinline__ int total_kblocks(const KParams& p, int g) {
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-__device__ __forceinline__ float gelu_f(float z) {
-  return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f));
-}
-__device__ __forceinline__ float gelu_grad_f(float z) {
-  float cdf = 0.5f * (1.0f + erff(z * 0.70710678118654752f));
-  float pdf = 0.39894228040143268f * __expf(-0.5f * z * z);
-  return cdf + z * pdf;
+// GELU and its derivative from one exponential: Phi(z) = 0.5 (1 + erf(z/sqrt2))
+// with erf by Abramowitz-Stegun 7.1.26 (|error| <= 1.5e-7, i.e. fp32-exact
+// for bf16 outputs): erf(x) = 1 - poly(t) e^{-x^2}, t = 1 / (1 + p x), x >= 0.
+// e^{-z^2/2} is both that exponential and sqrt(2 pi) * phi(z), so
+//   gelu(z) = z Phi(z),  gelu'(z) = Phi(z) + z phi(z)
+// cost 2 MUFU (rcp, ex2) + ~12 FMA instead of erff + expf per value.
+__device__ __forceinline__ void gelu_and_grad(float z, float& h, float& g) {
+  const float x = fabsf(z) * 0.70710678118654752f;
+  const float t = __fdividef(1.0f, fmaf(0.3275911f, x, 1.0f));
+  float poly = fmaf(1.061405429f, t, -1.453152027f);
+  poly = fmaf(poly, t, 1.421413741f);
+  poly = fmaf(poly, t, -0.284496736f);
+  poly = fmaf(poly, t, 0.254829592f);
+  poly *= t;
+  const float e = __expf(-0.5f * z * z);
+  const float tail = 0.5f * poly * e;  // 0.5 (1 - erf(x))
+  const float cdf = z >= 0.f ? 1.0f - tail : tail;
+  h = z * cdf;
+  g = fmaf(z * 0.39894228040143268f, e, cdf);
 }
 __device__ __forceinline__ float sigmoid_f(float z) { return 1.0f / (1.0f + __expf(-z)); }
 
@@ -128,6 +142,27 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
   }
 }
 
+// Epilogue staging. tcgen05.ld 32x32b gives each lane one accumulator ROW,
+// so direct stores put 32 different rows in every warp instruction (16 B per
+// row): ~1.3 TB/s into local HBM and ~165 GB/s over NVLink (tools/p2p_probe).
+// A warp instead stages a 32-row x 128-byte fragment in shared memory (XOR
+// swizzled by row, conflict-free) and writes it back with 8 lanes per row:
+// every instruction stores 4 contiguous 128-byte row segments.
+__device__ __forceinline__ void stage_store(uint4* stg, const uint4 (&w)[8], char* dst0,
+                                            long long ld_bytes, int lane, int nrow) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) stg[lane * 8 + (k ^ (lane & 7))] = w[k];
+  __syncwarp();
+  const int kk = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rr = i * 4 + (lane >> 3);
+    const uint4 v = stg[rr * 8 + (kk ^ (rr & 7))];
+    if (rr < nrow) *reinterpret_cast<uint4*>(dst0 + rr * ld_bytes + kk * 16) = v;
+  }
+  __syncwarp();
+}
+
 // CTAS = 1: one CTA computes a 128 x 256 tile (tcgen05 cta_group::1).
 // CTAS = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
 // with cta_group::2: each CTA stages its 128 rows of A and 128 of the 256
@@ -140,7 +175,9 @@ struct TileCfg {
   static constexpr int B_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int NSTAGE = CTAS == 1 ? 4 : 6;
-  static constexpr int SMEM = NSTAGE * STAGE + 1024 + 256;
+  static constexpr int STG_OFF = NSTAGE * STAGE + 256;         // epilogue staging
+  static constexpr int STG_BYTES = (EPI_THREADS / 32) * 4096;   // 4 KB per epilogue warp
+  static constexpr int SMEM = NSTAGE * STAGE + 1024 + 256 + STG_BYTES;
 };
 
 template <int CTAS>
@@ -359,6 +396,73 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             store_bf16x32(H + hcol, h);
           }
         }
+      } else if (p.epi == static_cast<int>(Epi::SwigluBwd)) {
+        // acc = dH over H units; dZ at the interleaved gate/up columns
+        const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
+        __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
+        for (int c = 4 * half; c < 4 * half + 4; ++c) {
+          const int col = ti.nt * BN + c * 32;
+          if (nkb > 0) {
+            tmem_ld_32x32b_x32(tbase + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          if (!row_ok || col >= p.out_cols) continue;
+          const int gcol = (col / 128) * 256 + (col % 128);
+          float g[32], u[32];
+          load_bf16x32(Z + gcol, g);
+          load_bf16x32(Z + gcol + 128, u);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float sg = sigmoid_f(g[i]);
+            const float silu = g[i] * sg;
+            const float dg = v[i] * u[i] * sg * (1.0f + g[i] * (1.0f - sg));
+            u[i] = v[i] * silu;
+            g[i] = dg;
+          }
+          store_bf16x32(dZ + gcol, g);
+          store_bf16x32(dZ + gcol + 128, u);
+        }
+      } else if (p.use_peers && p.epi == static_cast<int>(Epi::StoreBF16)) {
+        // Rows bound for other GPUs: stage so each NVLink store carries whole
+        // 128-byte row segments (direct 16-byte-per-row stores reach ~165 GB/s
+        // over NVLink, staged ones ~550; tools/p2p_probe.cu). Local outputs
+        // keep direct stores: the staging round trip costs more than it saves
+        // while the MMAs are reading shared memory.
+        uint4* stg = reinterpret_cast<uint4*>(smem + Cfg::STG_OFF) + (warp - 4) * 256;
+        const int r0 = ti.mt * Cfg::BM + static_cast<int>(rank) * 128 + q * 32;
+        const int nrow = min(max(p.out_rows - r0, 0), 32);
+        char* dst0 = fsmoe_dev::peer_row(p.peers, orow - lane, p.ldd * 2);
+        for (int cp = 0; cp < 2; ++cp) {
+          const int c = 4 * half + 2 * cp;
+          const int col = ti.nt * BN + c * 32;
+          if (col >= p.out_cols) continue;  // warp-uniform
+          uint4 w[8];
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            if (nkb > 0) {
+              tmem_ld_32x32b_x32(tbase + (c + hh) * 32, r);
+              tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 h[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                h[j] = __floats2bfloat162_rn(__uint_as_float(r[i * 8 + 2 * j]),
+                                             __uint_as_float(r[i * 8 + 2 * j + 1]));
+              w[4 * hh + i] = *reinterpret_cast<uint4*>(h);
+            }
+          }
+          stage_store(stg, w, dst0 + col * 2LL, p.ldd * 2, lane, nrow);
+        }
       } else {
         for (int c = 4 * half; c < 4 * half + 4; ++c) {
           const int col = ti.nt * BN + c * 32;
@@ -379,7 +483,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               break;
             }
             case static_cast<int>(Epi::StoreF32): {
-              float* D = static_cast<float*>(p.D) + orow * p.ldd + col;
+              float* D = (p.use_peers ? reinterpret_cast<float*>(fsmoe_dev::peer_row(p.peers, orow, p.ldd * 4))
+                                      : static_cast<float*>(p.D) + orow * p.ldd) + col;
               float4* d4 = reinterpret_cast<float4*>(D);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -393,41 +498,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               break;
             }
             case static_cast<int>(Epi::GeluFwd): {
-              __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
+              // D = gelu'(Z) (saved for the backward), D2 = H = gelu(Z)
+              __nv_bfloat16* G = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
               __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) + orow * p.ldd2;
-              store_bf16x32(Z + col, v);
-              float h[32];
+              float g[32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) h[i] = gelu_f(bf2f(__float2bfloat16(v[i])));
-              store_bf16x32(H + col, h);
+              for (int i = 0; i < 32; ++i) gelu_and_grad(bf2f(__float2bfloat16(v[i])), v[i], g[i]);
+              store_bf16x32(G + col, g);
+              store_bf16x32(H + col, v);
               break;
             }
             case static_cast<int>(Epi::GeluBwd): {
-              const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
+              const __nv_bfloat16* G = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
               __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-              float z[32];
-              load_bf16x32(Z + col, z);
+              float g[32];
+              load_bf16x32(G + col, g);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(z[i]);
+              for (int i = 0; i < 32; ++i) v[i] *= g[i];
               store_bf16x32(dZ + col, v);
-              break;
-            }
-            case static_cast<int>(Epi::SwigluBwd): {
-              const int gcol = (col / 128) * 256 + (col % 128);
-              const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
-              __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-              float g[32], u[32], dg[32];
-              load_bf16x32(Z + gcol, g);
-              load_bf16x32(Z + gcol + 128, u);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                float sg = sigmoid_f(g[i]);
-                float silu = g[i] * sg;
-                dg[i] = v[i] * u[i] * sg * (1.0f + g[i] * (1.0f - sg));
-                u[i] = v[i] * silu;
-              }
-              store_bf16x32(dZ + gcol, dg);
-              store_bf16x32(dZ + gcol + 128, u);
               break;
             }
             default:
@@ -520,6 +608,8 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.ldd2 = pr.ldd2;
   p.ldz = pr.ldz;
   p.accumulate = pr.accumulate ? 1 : 0;
+  p.use_peers = pr.use_peers ? 1 : 0;
+  p.peers = pr.peers;
   p.rows_total = pr.rows_total > 0 ? pr.rows_total : pr.rows;
   p.row0 = pr.row0;
   if (pr.nblk <= 0 || pr.rows <= 0) return cudaSuccess;

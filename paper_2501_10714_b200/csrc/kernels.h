@@ -6,8 +6,28 @@
 #include <cstddef>
 
 #include "../../include/fsmoe_cuda.h"
+#include "route_common.cuh"
 
 namespace fsmoe {
+
+// ABI peer map -> kernel argument; a plain buffer is the one-rank identity.
+inline fsmoe_dev::PeerRows peer_rows_of(const fsmoe_peer_rows* m) {
+  fsmoe_dev::PeerRows r{};
+  r.world = m->world;
+  r.rank = m->rank;
+  r.el = m->experts_local;
+  r.cap = m->capacity;
+  for (int i = 0; i < fsmoe_dev::MAX_PEERS; ++i) r.base[i] = static_cast<char*>(m->base[i]);
+  return r;
+}
+inline fsmoe_dev::PeerRows local_rows(void* buf) {
+  fsmoe_dev::PeerRows r{};
+  r.world = 1;
+  r.el = 1;
+  r.cap = 1;
+  r.base[0] = static_cast<char*>(buf);
+  return r;
+}
 
 size_t gate_workspace_bytes(const fsmoe_gate_desc& d);
 int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
@@ -41,7 +61,7 @@ int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, in
                        void* ws, cudaStream_t st);
 
 int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int* pick_of_slot,
-                    const int* ptok, const void* x, void* buf, cudaStream_t st);
+                    const int* ptok, const void* x, const fsmoe_dev::PeerRows& buf, cudaStream_t st);
 int combine_launch(int dtype, int T, int M, int E, long long C, int chunks, const int* tptr,
                    const int* tpick, const int* slot_of_pick, const double* pw, const void* buf,
                    void* y, cudaStream_t st);
@@ -50,6 +70,7 @@ int dispatch_bwd_launch(int dtype, int T, int M, int E, long long C, int chunks,
                         int accumulate, cudaStream_t st);
 int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long long P,
                        const int* pick_of_slot, const int* ptok, const double* pw,
-                       const void* dy, const void* buf, void* dbuf, double* dw, cudaStream_t st);
+                       const void* dy, const void* buf, const fsmoe_dev::PeerRows& dbuf, double* dw,
+                       cudaStream_t st);
 
 }  // namespace fsmoe

@@ -1,0 +1,141 @@
+// peer.cu — arrival flags for the peer-memory AlltoAll (include/fsmoe_cuda.h
+// fsmoe_peer_signal / fsmoe_peer_wait).
+//
+// The MoE layer's dispatch / combine exchanges are stores into the owning
+// rank's buffers, issued by the producing kernel itself over NVLink
+// (CUDA-IPC-mapped peer pointers). What remains of the "collective" is one
+// ordering edge per exchange: the producer's stream raises flag[slot][rank]
+// on every peer after its data stores, the consumer's stream spins until all
+// sources have raised flag[slot][*] to the exchange's sequence number.
+//
+//   signal:  (optional small payload rows) -> bar.sync -> fence.sc.sys ->
+//            red.release.sys.add(flag, 1)          one thread per peer
+//   wait:    ld.acquire.sys(flag) >= target        one thread per source
+//
+// The stores of the kernels before `signal` in stream order are complete at
+// its start (kernel boundary); the system-scope fence orders them, and the
+// payload, before the flag for the remote observer. Counters only grow, so a
+// flag is never reset and a late waiter cannot miss an increment.
+//
+// A peer that never signals (crashed rank) would spin the waiter forever; the
+// wait gives up after FSMOE_PEER_TIMEOUT_NS and traps so the process fails
+// instead of wedging the GPU.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "capi_common.h"
+#include "kernels.h"
+
+namespace fsmoe {
+namespace {
+
+using namespace fsmoe_dev;
+
+constexpr unsigned long long PEER_TIMEOUT_NS = 30ULL * 1000 * 1000 * 1000;
+
+struct Flags {
+  unsigned long long* base[MAX_PEERS];
+  int world, rank, nslots;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void peer_signal_kernel(Flags f, int slot, const unsigned long long* __restrict__ put,
+                                   int put_words, PeerRows put_dst, int put_rows) {
+  // payload: rows of put_words 8-byte words, [world][el] rows, capacity 1
+  const long long total = static_cast<long long>(put_rows) * put_words;
+  for (long long i = threadIdx.x; i < total; i += blockDim.x) {
+    const long long r = i / put_words;
+    const int w = static_cast<int>(i - r * put_words);
+    unsigned long long* d =
+        reinterpret_cast<unsigned long long*>(peer_row(put_dst, r, 8LL * put_words));
+    d[w] = put[i];
+  }
+  __syncthreads();
+  const int p = threadIdx.x;
+  if (p < f.world) {
+    __threadfence_system();
+    red_release_sys_add(f.base[p] + static_cast<long long>(slot) * f.world + f.rank, 1ULL);
+  }
+}
+
+__global__ void peer_wait_kernel(const unsigned long long* __restrict__ flags, int world, int slot,
+                                 unsigned long long target) {
+  const int src = threadIdx.x;
+  if (src < world) {
+    const unsigned long long* fl = flags + static_cast<long long>(slot) * world + src;
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(fl) < target) {
+      __nanosleep(64);
+      if (global_ns() - t0 > PEER_TIMEOUT_NS) {
+        printf("fsmoe_peer_wait: rank-%d flag of slot %d stuck below %llu (peer lost?)\n", src,
+               slot, target);
+        __trap();
+      }
+    }
+  }
+  __syncthreads();
+}
+
+int check_flags(const fsmoe_peer_flags* f, int slot) {
+  if (!f) return config_error("peer flags: null");
+  if (f->world < 1 || f->world > MAX_PEERS || f->rank < 0 || f->rank >= f->world)
+    return config_error("peer flags: world must be in [1, 8] and rank in [0, world)");
+  if (slot < 0 || slot >= f->nslots) return config_error("peer flags: slot out of range");
+  for (int p = 0; p < f->world; ++p)
+    if (!f->base[p]) return config_error("peer flags: missing peer flag array");
+  return FSMOE_OK;
+}
+
+}  // namespace
+}  // namespace fsmoe
+
+using namespace fsmoe;
+
+extern "C" int fsmoe_peer_signal(const fsmoe_peer_flags* f, int slot, const void* put_src,
+                                 long long put_row_bytes, const fsmoe_peer_rows* put_dst,
+                                 void* stream) {
+  if (int rc = check_flags(f, slot)) return rc;
+  Flags k{};
+  for (int p = 0; p < f->world; ++p) k.base[p] = f->base[p];
+  k.world = f->world;
+  k.rank = f->rank;
+  k.nslots = f->nslots;
+  fsmoe_dev::PeerRows dst{};
+  int rows = 0, words = 0;
+  if (put_src) {
+    if (!put_dst || put_row_bytes <= 0 || put_row_bytes % 8 || put_dst->capacity != 1)
+      return config_error("peer signal: payload rows must be 8-byte words with a capacity-1 map");
+    dst = peer_rows_of(put_dst);
+    rows = put_dst->world * put_dst->experts_local;
+    words = static_cast<int>(put_row_bytes / 8);
+  }
+  peer_signal_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      k, slot, static_cast<const unsigned long long*>(put_src), words, dst, rows);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "fsmoe_peer_signal");
+}
+
+extern "C" int fsmoe_peer_wait(const fsmoe_peer_flags* f, int slot, unsigned long long target,
+                               void* stream) {
+  if (int rc = check_flags(f, slot)) return rc;
+  peer_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(f->base[f->rank], f->world, slot,
+                                                                  target);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "fsmoe_peer_wait");
+}

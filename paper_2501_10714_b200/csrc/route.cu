@@ -203,12 +203,13 @@ template <typename V>
 __global__ void __launch_bounds__(256)
     dispatch_kernel(long long n_slots, int row_vecs, int E, long long C, int chunks,
                     const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
-                    const V* __restrict__ x, V* __restrict__ buf) {
+                    const V* __restrict__ x, const PeerRows buf) {
   const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (s >= n_slots) return;
   const int lane = threadIdx.x & 31;
   const int p = pick_of_slot[s];
-  V* dst = buf + slot_row(s, E, C, chunks) * row_vecs;
+  V* dst = reinterpret_cast<V*>(
+      peer_row(buf, slot_row(s, E, C, chunks), static_cast<long long>(row_vecs) * sizeof(V)));
   if (p < 0) {
     V z;
     memset(&z, 0, sizeof(V));
@@ -424,14 +425,14 @@ __global__ void __launch_bounds__(256)
     combine_bwd_kernel(long long n_slots, int M, int E, long long C, int chunks,
                        const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
                        const double* __restrict__ pw, const T* __restrict__ dy,
-                       const T* __restrict__ buf, T* __restrict__ dbuf, double* __restrict__ dw) {
+                       const T* __restrict__ buf, const PeerRows dbuf, double* __restrict__ dw) {
   using A = typename Acc<T>::type;
   const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (s >= n_slots) return;
   const int lane = threadIdx.x & 31;
   const int p = pick_of_slot[s];
   const long long row = slot_row(s, E, C, chunks);
-  T* dr = dbuf + row * M;
+  T* dr = reinterpret_cast<T*>(peer_row(dbuf, row, static_cast<long long>(M) * sizeof(T)));
   if (p < 0) {
     A z[CV];
 #pragma unroll
@@ -533,7 +534,7 @@ int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, in
 }
 
 int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int* pick_of_slot,
-                    const int* ptok, const void* x, void* buf, cudaStream_t st) {
+                    const int* ptok, const void* x, const PeerRows& buf, cudaStream_t st) {
   const long long n_slots = static_cast<long long>(E) * C;
   if (n_slots <= 0 || M <= 0) return FSMOE_OK;
   const long long row_bytes = static_cast<long long>(M) * elem_size(dtype);
@@ -541,15 +542,15 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
   if (row_bytes % 16 == 0) {
     dispatch_kernel<uint4><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 16), E, C,
                                                  chunks, pick_of_slot, ptok,
-                                                 static_cast<const uint4*>(x), static_cast<uint4*>(buf)); ::fsmoe::count_launch();
+                                                 static_cast<const uint4*>(x), buf); ::fsmoe::count_launch();
   } else if (row_bytes % 8 == 0) {
     dispatch_kernel<uint2><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 8), E, C,
                                                  chunks, pick_of_slot, ptok,
-                                                 static_cast<const uint2*>(x), static_cast<uint2*>(buf)); ::fsmoe::count_launch();
+                                                 static_cast<const uint2*>(x), buf); ::fsmoe::count_launch();
   } else {
     dispatch_kernel<uint16_t><<<grid, 256, 0, st>>>(
         n_slots, static_cast<int>(row_bytes / 2), E, C, chunks, pick_of_slot, ptok,
-        static_cast<const uint16_t*>(x), static_cast<uint16_t*>(buf)); ::fsmoe::count_launch();
+        static_cast<const uint16_t*>(x), buf); ::fsmoe::count_launch();
   }
   return cuda_status(cudaGetLastError(), "fsmoe_dispatch");
 }
@@ -596,7 +597,8 @@ int dispatch_bwd_launch(int dtype, int T, int M, int E, long long C, int chunks,
 
 int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long long P,
                        const int* pick_of_slot, const int* ptok, const double* pw,
-                       const void* dy, const void* buf, void* dbuf, double* dw, cudaStream_t st) {
+                       const void* dy, const void* buf, const PeerRows& dbuf, double* dw,
+                       cudaStream_t st) {
   const long long n_slots = static_cast<long long>(E) * C;
   if (P > 0) FSMOE_CUDA_TRY(cudaMemsetAsync(dw, 0, sizeof(double) * P, st), "combine_bwd memset");
   if (n_slots <= 0 || M <= 0) return FSMOE_OK;
@@ -607,12 +609,12 @@ int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long lo
       combine_bwd_kernel<Tt, true><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
                                                          static_cast<const Tt*>(dy),
                                                          static_cast<const Tt*>(buf),
-                                                         static_cast<Tt*>(dbuf), dw);
+                                                         dbuf, dw);
     else
       combine_bwd_kernel<Tt, false><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
                                                           static_cast<const Tt*>(dy),
                                                           static_cast<const Tt*>(buf),
-                                                          static_cast<Tt*>(dbuf), dw);
+                                                          dbuf, dw);
     ::fsmoe::count_launch();
   });
   if (rc) return config_error("combine_bwd: unknown dtype");

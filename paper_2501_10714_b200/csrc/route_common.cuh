@@ -45,6 +45,25 @@ __host__ __device__ __forceinline__ long long slot_row(long long slot, int exper
   return static_cast<long long>(experts) * lo + e * (hi - lo) + (c - lo);
 }
 
+// Destination of a row of a [P][E_l][C] block buffer written to peer memory
+// (include/fsmoe_cuda.h fsmoe_peer_rows): row r of block b = p*E_l + e_l goes
+// to base[p] at row (rank*E_l + e_l)*C + r%C -- the receiver's layout is the
+// same [P][E_l][C] indexed by source rank. world 1 / rank 0 is the identity.
+constexpr int MAX_PEERS = 8;
+struct PeerRows {
+  char* base[MAX_PEERS];
+  int world, rank, el;
+  long long cap;
+};
+__device__ __forceinline__ char* peer_row(const PeerRows& m, long long row, long long row_bytes) {
+  if (m.world <= 1) return m.base[0] + row * row_bytes;
+  const long long b = row / m.cap;
+  const long long c = row - b * m.cap;
+  const int p = static_cast<int>(b / m.el);
+  const long long e = b - static_cast<long long>(p) * m.el;
+  return m.base[p] + ((static_cast<long long>(m.rank) * m.el + e) * m.cap + c) * row_bytes;
+}
+
 // Monotone map double -> uint64 (a < b  <=>  key(a) < key(b)) for non-NaN.
 __device__ __forceinline__ uint64_t order_key(double v) {
   if (v == 0.0) v = 0.0;  // -0.0 == +0.0 in the reference's comparisons

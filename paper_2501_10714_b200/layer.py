@@ -205,6 +205,20 @@ class MoELayer:
         NL.check(lib.fsmoe_layer_backward(self.h, _p(dy), _p(dx), self._stream()), lib)
         return dx
 
+    def set_trace(self, on: bool = True):
+        """Record a measured per-phase timeline on both streams (synchronises)."""
+        lib = NL.cpp_lib()
+        NL.check(lib.fsmoe_layer_set_trace(self.h, 1 if on else 0), lib)
+
+    def trace_json(self) -> str:
+        """Chrome-trace JSON of the traced calls since set_trace(True)."""
+        lib = NL.cpp_lib()
+        lib.fsmoe_layer_trace.restype = C.c_longlong
+        n = lib.fsmoe_layer_trace(self.h, None, 0)
+        buf = C.create_string_buffer(n)
+        lib.fsmoe_layer_trace(self.h, buf, n)
+        return buf.value.decode()
+
     def buffer(self, name, dtype, shape=None):
         """View of a named internal device buffer (tests / inspection)."""
         lib = NL.cpp_lib()

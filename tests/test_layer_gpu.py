@@ -100,3 +100,29 @@ def test_config1_shape_check_mode():
     assert _rel(layer.g_w1, ref["g_w1"]) < 1e-4
     assert _rel(layer.g_w2, ref["g_w2"]) < 1e-4
     assert _rel(layer.g_gate, ref["g_gate"]) < 1e-4
+
+
+def test_trace_timeline_has_every_phase_and_same_results():
+    """The measured timeline (fsmoe_layer_trace) records every simulator task
+    kind and tracing does not change the results."""
+    import json
+    from paper_2501_10714_b200.layer import MoEConfig, MoELayer
+    cfg = MoEConfig(tokens=512, model_dim=256, ffn_dim=256, experts=8, top_k=2, r_fwd=2, r_bwd=2)
+    layer = MoELayer(cfg, init_seed=3)
+    g = torch.Generator().manual_seed(5)
+    x = (torch.rand(512, 256, generator=g) * 2 - 1).to("cuda", torch.bfloat16)
+    dy = (torch.rand(512, 256, generator=g) * 2 - 1).to("cuda", torch.bfloat16)
+    y0 = layer.forward(x).clone()
+    dx0 = layer.backward(dy).clone()
+    layer.set_trace(True)
+    y1 = layer.forward(x).clone()
+    dx1 = layer.backward(dy).clone()
+    tr = json.loads(layer.trace_json())
+    layer.set_trace(False)
+    assert torch.equal(y0, y1) and torch.equal(dx0, dx1)
+    names = {e["name"] for e in tr["traceEvents"]}
+    for n in ("fwd.gate", "fwd.order", "fwd.expert[0]", "fwd.i-order",
+              "bwd.i-order", "bwd.expert[0]", "bwd.order", "bwd.gate"):
+        assert n in names, (n, names)
+    assert all(e["dur"] >= 0 and e["ts"] >= 0 for e in tr["traceEvents"])
+    layer.close()
