@@ -30,4 +30,5 @@ def main(path, marker="rowdot", skip_steps=3):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    a = sys.argv[1:]
+    main(a[0], a[1] if len(a) > 1 else "rowdot", int(a[2]) if len(a) > 2 else 3)
