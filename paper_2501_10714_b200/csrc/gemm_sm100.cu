@@ -18,6 +18,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "gemm.h"
@@ -142,27 +143,6 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
   }
 }
 
-// Epilogue staging. tcgen05.ld 32x32b gives each lane one accumulator ROW,
-// so direct stores put 32 different rows in every warp instruction (16 B per
-// row): ~1.3 TB/s into local HBM and ~165 GB/s over NVLink (tools/p2p_probe).
-// A warp instead stages a 32-row x 128-byte fragment in shared memory (XOR
-// swizzled by row, conflict-free) and writes it back with 8 lanes per row:
-// every instruction stores 4 contiguous 128-byte row segments.
-__device__ __forceinline__ void stage_store(uint4* stg, const uint4 (&w)[8], char* dst0,
-                                            long long ld_bytes, int lane, int nrow) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k) stg[lane * 8 + (k ^ (lane & 7))] = w[k];
-  __syncwarp();
-  const int kk = lane & 7;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int rr = i * 4 + (lane >> 3);
-    const uint4 v = stg[rr * 8 + (kk ^ (rr & 7))];
-    if (rr < nrow) *reinterpret_cast<uint4*>(dst0 + rr * ld_bytes + kk * 16) = v;
-  }
-  __syncwarp();
-}
-
 // CTAS = 1: one CTA computes a 128 x 256 tile (tcgen05 cta_group::1).
 // CTAS = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
 // with cta_group::2: each CTA stages its 128 rows of A and 128 of the 256
@@ -174,10 +154,18 @@ struct TileCfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NSTAGE = CTAS == 1 ? 4 : 6;
-  static constexpr int STG_OFF = NSTAGE * STAGE + 256;         // epilogue staging
-  static constexpr int STG_BYTES = (EPI_THREADS / 32) * 4096;   // 4 KB per epilogue warp
-  static constexpr int SMEM = NSTAGE * STAGE + 1024 + 256 + STG_BYTES;
+  static constexpr int NSTAGE = CTAS == 1 ? 3 : 5;
+  static constexpr int STG_OFF = NSTAGE * STAGE + 1024;         // after the barrier block
+  static constexpr int STG_PER_WARP = 8192;                     // two 4 KB SW128 boxes
+  static constexpr int SMEM = STG_OFF + (EPI_THREADS / 32) * STG_PER_WARP + 1024;
+};
+
+// Epilogue tensor maps (TMA stores / loads of 32-row x 128-byte SW128 boxes):
+// d = main output, d2 = GeluFwd's H, z = GeluBwd's saved gelu', peer[p] =
+// rank p's receive buffer when the output rows belong to other GPUs.
+struct EpiMaps {
+  CUtensorMap d, d2, z;
+  CUtensorMap peer[fsmoe_dev::MAX_PEERS];
 };
 
 template <int CTAS>
@@ -195,7 +183,8 @@ __device__ __forceinline__ TileInfo decode_tile_c(const KParams& p, int t) {
 template <int CTAS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const KParams p) {
+                        const __grid_constant__ CUtensorMap tmB, const KParams p,
+                        const __grid_constant__ EpiMaps em) {
   using Cfg = TileCfg<CTAS>;
   constexpr int NS = Cfg::NSTAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -206,6 +195,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + NS;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* zbar = tempty_bar + 3;        // [8 epilogue warps][2 boxes]: GeluBwd loads
 
   const int warp = threadIdx.x / 32;
   const bool a_mn = (p.kind == 1);
@@ -226,6 +216,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], (EPI_THREADS / 32) * CTAS);  // one arrive per epilogue warp
     }
+    for (int i = 0; i < 2 * (EPI_THREADS / 32); ++i) mbar_init(&zbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -342,19 +333,62 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue (every CTA: its 128 TMEM lanes) ========
+    // Warp (q, half) owns accumulator rows [32q, 32q+32) of this CTA and
+    // columns [128 half, 128 half + 128) of the tile. Outputs leave through
+    // TMA: the warp writes a 32-row x 128-byte box into shared memory in the
+    // SW128 layout (16-byte unit k of row r at k ^ (r & 7): conflict-free with
+    // one row per lane) and one lane issues the tensor store (or, for
+    // accumulating fp32 wgrad outputs, the tensor reduce-add). Two boxes per
+    // warp alternate so the next box is written while the last is in flight.
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;  // which 128 accumulator columns
+    const int half = (warp - 4) >> 2;
     const int lane = threadIdx.x & 31;
+    const int wi = warp - 4;
+    uint8_t* stg = smem + Cfg::STG_OFF + wi * Cfg::STG_PER_WARP;
+    uint64_t* zb = zbar + 2 * wi;
+    uint32_t zph[2] = {0u, 0u};
     const uint32_t tempty_leader = mapa_shared(&tempty_bar[0], 0);
+    const bool tma_epi = p.epi == static_cast<int>(Epi::StoreBF16) ||
+                         p.epi == static_cast<int>(Epi::StoreF32) ||
+                         p.epi == static_cast<int>(Epi::GeluFwd) ||
+                         p.epi == static_cast<int>(Epi::GeluBwd);
+    // this lane's row inside a box: unit k of the row lives at (k ^ (lane & 7))
+    auto box_row = [&](uint8_t* box) { return reinterpret_cast<uint4*>(box + lane * 128); };
+    const int sw = lane & 7;
     int acc = 0;
     uint32_t aph = 0;
     for (int t = unit; t < p.num_tiles; t += nunits) {
       TileInfo ti = decode_tile_c<CTAS>(p, t);
       if (ti.skip) continue;
       const int nkb = total_kblocks(p, ti.g);
+      const int rloc = ti.mt * Cfg::BM + static_cast<int>(rank) * 128 + q * 32;  // first row of the warp
+      // TMA box coordinates of the warp's rows: (col, row, block)
+      int c1 = p.kind == 0 ? p.row0 + rloc : rloc;
+      int c2 = ti.g;
+      const CUtensorMap* md = &em.d;
+      if (p.use_peers) {
+        const int pp = ti.g / p.peers.el;
+        c2 = p.peers.rank * p.peers.el + (ti.g - pp * p.peers.el);
+        md = &em.peer[pp];
+      }
+      if (p.epi == static_cast<int>(Epi::GeluBwd)) {
+        // prefetch this warp's saved gelu'(Z) boxes while the MMAs still run
+        if (lane == 0) {
+          bulk_wait_read<0>();  // the previous tile's stores have left the boxes
+#pragma unroll
+          for (int pc = 0; pc < 2; ++pc) {
+            const int col = ti.nt * BN + (4 * half + 2 * pc) * 32;
+            if (col < p.out_cols) {
+              mbar_arrive_expect_tx(&zb[pc], 4096);
+              tma_load_3d(stg + pc * 4096, &em.z, &zb[pc], col, c1, ti.g);
+            }
+          }
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull_bar[acc], aph);
       tc_fence_after();
-      const int row = ti.mt * Cfg::BM + static_cast<int>(rank) * 128 + q * 32 + lane;
+      const int row = rloc + lane;
       const bool row_ok = row < p.out_rows;
       const long long orow = p.kind == 0
                                  ? static_cast<long long>(ti.g) * p.rows_total + p.row0 + row
@@ -362,7 +396,113 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       uint32_t r[32];
       float v[32];
-      if (p.epi == static_cast<int>(Epi::SwigluFwd)) {
+      if (tma_epi && p.epi == static_cast<int>(Epi::StoreF32)) {
+        // fp32: one 32-column TMEM chunk = one box
+        for (int c = 4 * half; c < 4 * half + 4; ++c) {
+          const int col = ti.nt * BN + c * 32;
+          if (nkb > 0) {
+            tmem_ld_32x32b_x32(tbase + c * 32, r);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+          }
+          if (col >= p.out_cols) continue;  // warp-uniform
+          uint8_t* box = stg + (c & 1) * 4096;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          uint4* br = box_row(box);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) br[k ^ sw] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.accumulate) tma_reduce_add_3d(md, box, col, c1, c2);
+            else tma_store_3d(md, box, col, c1, c2);
+            bulk_commit();
+          }
+        }
+      } else if (tma_epi) {
+        // bf16: two TMEM chunks (64 columns) = one box
+        for (int pc = 0; pc < 2; ++pc) {
+          const int c = 4 * half + 2 * pc;
+          const int col = ti.nt * BN + c * 32;
+          if (col >= p.out_cols) continue;  // warp-uniform
+          uint32_t r2[32];
+          if (nkb > 0) {
+            tmem_ld_32x32b_x32(tbase + c * 32, r);
+            tmem_ld_32x32b_x32(tbase + (c + 1) * 32, r2);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = r2[i] = 0u;
+          }
+          auto pk = [&](float a, float b) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+            return *reinterpret_cast<uint32_t*>(&h);
+          };
+          auto val = [&](int i) { return __uint_as_float(i < 32 ? r[i] : r2[i - 32]); };
+          if (p.epi == static_cast<int>(Epi::StoreBF16)) {
+            uint8_t* box = stg + pc * 4096;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint4* br = box_row(box);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              br[k ^ sw] = make_uint4(pk(val(8 * k), val(8 * k + 1)), pk(val(8 * k + 2), val(8 * k + 3)),
+                                      pk(val(8 * k + 4), val(8 * k + 5)), pk(val(8 * k + 6), val(8 * k + 7)));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(md, box, col, c1, c2);
+              bulk_commit();
+            }
+          } else if (p.epi == static_cast<int>(Epi::GeluFwd)) {
+            // box 0: gelu'(Z) (saved for the backward), box 1: H = gelu(Z)
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+            uint4* bg = box_row(stg);
+            uint4* bh = box_row(stg + 4096);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              float h[8], g[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) gelu_and_grad(bf2f(__float2bfloat16(val(8 * k + j))), h[j], g[j]);
+              bg[k ^ sw] = make_uint4(pk(g[0], g[1]), pk(g[2], g[3]), pk(g[4], g[5]), pk(g[6], g[7]));
+              bh[k ^ sw] = make_uint4(pk(h[0], h[1]), pk(h[2], h[3]), pk(h[4], h[5]), pk(h[6], h[7]));
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(md, stg, col, c1, c2);
+              tma_store_3d(&em.d2, stg + 4096, col, c1, c2);
+              bulk_commit();
+            }
+          } else {  // GeluBwd: dZ = dH * gelu'(Z), written over the loaded box
+            uint8_t* box = stg + pc * 4096;
+            mbar_wait(&zb[pc], zph[pc]);
+            zph[pc] ^= 1u;
+            uint4* br = box_row(box);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              uint4 gw = br[k ^ sw];
+              const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gw);
+              float2 g0 = __bfloat1622float2(g2[0]), g1 = __bfloat1622float2(g2[1]);
+              float2 g2f = __bfloat1622float2(g2[2]), g3 = __bfloat1622float2(g2[3]);
+              br[k ^ sw] = make_uint4(pk(val(8 * k) * g0.x, val(8 * k + 1) * g0.y),
+                                      pk(val(8 * k + 2) * g1.x, val(8 * k + 3) * g1.y),
+                                      pk(val(8 * k + 4) * g2f.x, val(8 * k + 5) * g2f.y),
+                                      pk(val(8 * k + 6) * g3.x, val(8 * k + 7) * g3.y));
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(md, box, col, c1, c2);
+              bulk_commit();
+            }
+          }
+        }
+      } else if (p.epi == static_cast<int>(Epi::SwigluFwd)) {
         // tile cols: [0,128) gate units, [128,256) up units (same 128 units)
         __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
         __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) + orow * p.ldd2;
@@ -396,8 +536,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             store_bf16x32(H + hcol, h);
           }
         }
-      } else if (p.epi == static_cast<int>(Epi::SwigluBwd)) {
-        // acc = dH over H units; dZ at the interleaved gate/up columns
+      } else {  // SwigluBwd: acc = dH over H units; dZ at the interleaved gate/up columns
         const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
         __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
         for (int c = 4 * half; c < 4 * half + 4; ++c) {
@@ -427,101 +566,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           store_bf16x32(dZ + gcol, g);
           store_bf16x32(dZ + gcol + 128, u);
         }
-      } else if (p.use_peers && p.epi == static_cast<int>(Epi::StoreBF16)) {
-        // Rows bound for other GPUs: stage so each NVLink store carries whole
-        // 128-byte row segments (direct 16-byte-per-row stores reach ~165 GB/s
-        // over NVLink, staged ones ~550; tools/p2p_probe.cu). Local outputs
-        // keep direct stores: the staging round trip costs more than it saves
-        // while the MMAs are reading shared memory.
-        uint4* stg = reinterpret_cast<uint4*>(smem + Cfg::STG_OFF) + (warp - 4) * 256;
-        const int r0 = ti.mt * Cfg::BM + static_cast<int>(rank) * 128 + q * 32;
-        const int nrow = min(max(p.out_rows - r0, 0), 32);
-        char* dst0 = fsmoe_dev::peer_row(p.peers, orow - lane, p.ldd * 2);
-        for (int cp = 0; cp < 2; ++cp) {
-          const int c = 4 * half + 2 * cp;
-          const int col = ti.nt * BN + c * 32;
-          if (col >= p.out_cols) continue;  // warp-uniform
-          uint4 w[8];
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            if (nkb > 0) {
-              tmem_ld_32x32b_x32(tbase + (c + hh) * 32, r);
-              tmem_ld_wait();
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) r[i] = 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              __nv_bfloat162 h[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                h[j] = __floats2bfloat162_rn(__uint_as_float(r[i * 8 + 2 * j]),
-                                             __uint_as_float(r[i * 8 + 2 * j + 1]));
-              w[4 * hh + i] = *reinterpret_cast<uint4*>(h);
-            }
-          }
-          stage_store(stg, w, dst0 + col * 2LL, p.ldd * 2, lane, nrow);
-        }
-      } else {
-        for (int c = 4 * half; c < 4 * half + 4; ++c) {
-          const int col = ti.nt * BN + c * 32;
-          if (nkb > 0) {
-            tmem_ld_32x32b_x32(tbase + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          if (!row_ok || col >= p.out_cols) continue;
-          switch (p.epi) {
-            case static_cast<int>(Epi::StoreBF16): {
-              __nv_bfloat16* D = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-              store_bf16x32(D + col, v);
-              break;
-            }
-            case static_cast<int>(Epi::StoreF32): {
-              float* D = (p.use_peers ? reinterpret_cast<float*>(fsmoe_dev::peer_row(p.peers, orow, p.ldd * 4))
-                                      : static_cast<float*>(p.D) + orow * p.ldd) + col;
-              float4* d4 = reinterpret_cast<float4*>(D);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                if (p.accumulate) {
-                  float4 e = d4[i];
-                  o.x += e.x; o.y += e.y; o.z += e.z; o.w += e.w;
-                }
-                d4[i] = o;
-              }
-              break;
-            }
-            case static_cast<int>(Epi::GeluFwd): {
-              // D = gelu'(Z) (saved for the backward), D2 = H = gelu(Z)
-              __nv_bfloat16* G = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-              __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) + orow * p.ldd2;
-              float g[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) gelu_and_grad(bf2f(__float2bfloat16(v[i])), v[i], g[i]);
-              store_bf16x32(G + col, g);
-              store_bf16x32(H + col, v);
-              break;
-            }
-            case static_cast<int>(Epi::GeluBwd): {
-              const __nv_bfloat16* G = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
-              __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-              float g[32];
-              load_bf16x32(G + col, g);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= g[i];
-              store_bf16x32(dZ + col, v);
-              break;
-            }
-            default:
-              break;
-          }
-        }
       }
       tc_fence_before();
       __syncwarp();
@@ -531,6 +575,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
+    if (lane == 0) bulk_wait<0>();  // outputs written before the kernel retires
+    __syncwarp();
   }
 
   tc_fence_before();
@@ -571,6 +617,23 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// General 3-D map: element type, dims {d0 (contiguous), d1, d2}, byte strides of
+// dims 1 and 2, box {b0, b1, 1}, 128-byte swizzle (the epilogue box layout).
+bool make_map3s(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_t d1, uint64_t d2,
+                uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b1) {
+  auto enc = get_encode_fn();
+  if (!enc || !base) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1, s2};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -651,6 +714,43 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     if (!make_map3(&tb, pr.B, pr.No, p.rows_total, pr.nblk, 64, BK)) return cudaErrorInvalidValue;
   }
   p.num_tiles = p.n_groups * p.m_tiles * p.n_tiles;
+  // epilogue maps: 32-row boxes of 128 bytes (64 bf16 / 32 fp32 columns); the
+  // row extent ends at the window so TMA clips rows outside [row0, row0+rows)
+  EpiMaps em;
+  memset(&em, 0, sizeof(em));
+  {
+    const bool f32 = pr.epi == Epi::StoreF32;
+    const uint64_t es = f32 ? 4 : 2;
+    const uint32_t bc = f32 ? 32 : 64;
+    const bool tma_epi = pr.epi == Epi::StoreBF16 || pr.epi == Epi::StoreF32 ||
+                         pr.epi == Epi::GeluFwd || pr.epi == Epi::GeluBwd;
+    if (tma_epi) {
+      if (pr.kind == GemmKind::RowGrouped) {
+        const uint64_t rows_end = static_cast<uint64_t>(p.row0) + pr.rows;
+        const uint64_t s1 = pr.ldd * es, s2 = static_cast<uint64_t>(p.rows_total) * pr.ldd * es;
+        if (pr.use_peers) {
+          const int blocks = pr.peers.world * pr.peers.el;
+          for (int pp = 0; pp < pr.peers.world; ++pp)
+            if (!make_map3s(&em.peer[pp], pr.peers.base[pp], f32, pr.N, rows_end, blocks, s1, s2, bc, 32))
+              return cudaErrorInvalidValue;
+        } else if (!make_map3s(&em.d, pr.D, f32, pr.N, rows_end, pr.nblk, s1, s2, bc, 32)) {
+          return cudaErrorInvalidValue;
+        }
+        if (pr.epi == Epi::GeluFwd &&
+            !make_map3s(&em.d2, pr.D2, false, pr.N, rows_end, pr.nblk, pr.ldd2 * 2,
+                        static_cast<uint64_t>(p.rows_total) * pr.ldd2 * 2, 64, 32))
+          return cudaErrorInvalidValue;
+        if (pr.epi == Epi::GeluBwd &&
+            !make_map3s(&em.z, pr.Zin, false, pr.N, rows_end, pr.nblk, pr.ldz * 2,
+                        static_cast<uint64_t>(p.rows_total) * pr.ldz * 2, 64, 32))
+          return cudaErrorInvalidValue;
+      } else {
+        if (!make_map3s(&em.d, pr.D, f32, pr.No, pr.Mo, p.n_w, pr.ldd * es,
+                        static_cast<uint64_t>(pr.Mo) * pr.ldd * es, bc, 32))
+          return cudaErrorInvalidValue;
+      }
+    }
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(grouped_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -662,7 +762,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   const int max_units = num_sms() / ctas;
   const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
   if (ctas == 1) {
-    grouped_gemm_kernel<1><<<units, NUM_THREADS, TileCfg<1>::SMEM, stream>>>(ta, tb, p);
+    grouped_gemm_kernel<1><<<units, NUM_THREADS, TileCfg<1>::SMEM, stream>>>(ta, tb, p, em);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(units * 2);
@@ -676,7 +776,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<2>, ta, tb, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<2>, ta, tb, p, em);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   ::fsmoe::count_launch();
