@@ -29,6 +29,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstdio>
+#include <algorithm>
+#include <vector>
 
 #include "capi_common.h"
 #include "kernels.h"
@@ -516,6 +520,484 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+
+// ===================================================================== fused
+// Two-kernel form of steps 2-7 for bf16 tokens, E <= 32 (the training hot
+// path): `screen_kernel` = approximate scores + norms + noise + bounds +
+// candidate masks for 64 tokens per block (no split-K partials, no T x E
+// bound arrays in HBM); `exact_final_kernel` = the exact fp64 logits of each
+// token's candidates and the final top-k / weights for 32 tokens per block
+// (no per-expert candidate lists). Same arithmetic, same bound, same results.
+
+constexpr int SC_TOK = 64;             // tokens per screen block
+constexpr int SC_JC = 64;              // reduction chunk (columns of x)
+constexpr int SC_XROW = SC_JC + 8;     // bf16 per smem x row: 144 B, conflict-free LDS.128
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
+                   __cvta_generic_to_shared(smem))),
+               "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int SC_FROW = SC_JC + 4;    // fp32 per smem x row (converted tile)
+
+// d = a * (b.x, b.y) + c, two IEEE fp32 FMAs in one FFMA2 (a broadcast)
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+  const float2 aa = make_float2(a, a);
+  unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&aa);
+  unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+  unsigned long long rc = *reinterpret_cast<const unsigned long long*>(&c);
+  unsigned long long rd;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  return *reinterpret_cast<float2*>(&rd);
+}
+
+template <int NCP, int E_MAX>
+struct ScreenSmem {
+  static constexpr int X = 2 * SC_TOK * SC_XROW * 2;       // bf16 x chunks, double-buffered
+  static constexpr int XF = SC_TOK * SC_FROW * 4;          // the current chunk in fp32
+  static constexpr int W = 2 * SC_JC * NCP * 4;            // fp32 W chunks
+  static constexpr int DRAWS = SC_TOK * 2 * E_MAX * 8;     // mt19937_64 outputs
+  static constexpr int LOHI = SC_TOK * E_MAX * 8 * 2;      // bounds
+  static constexpr int NRM = SC_TOK * 4 * 4;
+  static constexpr int BYTES = X + XF + W + DRAWS + LOHI + NRM;
+};
+
+// KIND 0 noisy (NC = 2E), 1 sigmoid (NC = E); NCP = NC rounded up to 32 / 64.
+// Two thread groups split each chunk's columns of x (in-block split-K: two
+// partial FMA chains per output, summed once; covered by the bound's split
+// term). Thread (g, tx, ty): columns 4tx..4tx+3, tokens ty + 16 i (i < 4).
+constexpr int SC_GRP = 4;  // in-block split-K groups
+
+template <int KIND, int NCP, int E_MAX>
+__global__ void __launch_bounds__(NCP * 4 * SC_GRP)
+    screen_kernel(const __nv_bfloat16* __restrict__ x, int T, int M, int E, int k,
+                  const float* __restrict__ W32, int NC, const double* __restrict__ wn, double cB,
+                  double gam, uint64_t seed, double* __restrict__ noise_ws,
+                  double* __restrict__ scores_out, double* __restrict__ spread_out,
+                  uint64_t* __restrict__ mask) {
+  using S = ScreenSmem<NCP, E_MAX>;
+  constexpr int NT = NCP * 4 * SC_GRP;
+  constexpr int QX = NCP / 4;  // column quads
+  extern __shared__ __align__(16) uint8_t sm[];
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);
+  float* xf = reinterpret_cast<float*>(sm + S::X);
+  float* wsm = reinterpret_cast<float*>(sm + S::X + S::XF);
+  uint64_t* draws = reinterpret_cast<uint64_t*>(sm + S::X + S::XF + S::W);
+  double* lo = reinterpret_cast<double*>(sm + S::X + S::XF + S::W + S::DRAWS);
+  double* hi = lo + SC_TOK * E_MAX;
+  float* nrm = reinterpret_cast<float*>(sm + S::X + S::XF + S::W + S::DRAWS + S::LOHI);
+  const int tid = threadIdx.x;
+  const int grp = tid / (NCP * 4), lt = tid % (NCP * 4);
+  const int tx = lt % QX, ty = lt / QX;
+  const int t0 = blockIdx.x * SC_TOK;
+  const int ntok = min(SC_TOK, T - t0);
+  // zero the padding columns of both W buffers once (cp.async only fills < NC)
+  if (NC < NCP)
+    for (int i = tid; i < 2 * SC_JC * NCP; i += NT)
+      if (i % NCP >= NC) wsm[i] = 0.f;
+  const int nck = M / SC_JC;
+  auto issue = [&](int ck) {
+    if (ck < nck) {
+      const int b = ck & 1;
+      const int j0 = ck * SC_JC;
+      for (int i = tid; i < SC_TOK * (SC_JC / 8); i += NT) {
+        const int r = i / (SC_JC / 8), c = i % (SC_JC / 8);
+        const int t = t0 + (r < ntok ? r : 0);
+        cp_async16(xs + (b * SC_TOK + r) * SC_XROW + c * 8, x + static_cast<long long>(t) * M + j0 + c * 8);
+      }
+      const int q = NC / 4;
+      for (int i = tid; i < SC_JC * q; i += NT) {
+        const int r = i / q, c = i % q;
+        cp_async16(wsm + (b * SC_JC + r) * NCP + c * 4, W32 + static_cast<long long>(j0 + r) * NC + c * 4);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  // noise draws of this block's tokens: the seeding recurrence is sequential
+  if (KIND == 0 && tid < ntok) {
+    uint64_t lw[2 * E_MAX + 1];
+    uint64_t w = seed + static_cast<uint64_t>(t0 + tid);
+    lw[0] = w;
+    const int nout = 2 * E;
+    for (int i = 1; i <= nout; ++i) {
+      w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+      lw[i] = w;
+    }
+    for (int i = nout + 1; i < 156; ++i) w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+    for (int o = 0; o < nout; ++o) {
+      w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(156 + o);
+      const uint64_t y = (lw[o] & MT_UM) | (lw[o + 1] & MT_LM);
+      draws[tid * 2 * E_MAX + o] = temper(w ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL));
+    }
+  }
+  float2 acc[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+  float nacc = 0.f;  // |x|^2 partial: token tid/4, quarter (tid&3) of each chunk
+  for (int ck = 0; ck < nck; ++ck) {
+    if (ck + 1 < nck) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    const int b = ck & 1;
+    // bf16 -> fp32 once per element (thread: token tid/4, quarter tid&3),
+    // |x|^2 from the exact squares of the bf16 values
+    if (tid < 4 * SC_TOK) {
+      const __nv_bfloat16* xr = xs + (b * SC_TOK + (tid >> 2)) * SC_XROW + (tid & 3) * (SC_JC / 4);
+      float* fr = xf + (tid >> 2) * SC_FROW + (tid & 3) * (SC_JC / 4);
+#pragma unroll
+      for (int j = 0; j < SC_JC / 4; j += 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(xr + j);
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[2 * q] = __uint_as_float(w4[q] << 16);
+          v[2 * q + 1] = __uint_as_float(w4[q] & 0xffff0000u);
+          nacc = fmaf(v[2 * q], v[2 * q], nacc);
+          nacc = fmaf(v[2 * q + 1], v[2 * q + 1], nacc);
+        }
+        *reinterpret_cast<float4*>(fr + j) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(fr + j + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      }
+    }
+    __syncthreads();
+    const float* wb = wsm + b * SC_JC * NCP;
+#pragma unroll 2
+    for (int j4 = grp * (SC_JC / 4 / SC_GRP); j4 < (grp + 1) * (SC_JC / 4 / SC_GRP); ++j4) {
+      float4 xv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const float4*>(xf + (ty + 16 * i) * SC_FROW + j4 * 4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wb + (j4 * 4 + q) * NCP + 4 * tx);
+        const float2 wl = make_float2(w4.x, w4.y), wh = make_float2(w4.z, w4.w);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float xq = q == 0 ? xv[i].x : q == 1 ? xv[i].y : q == 2 ? xv[i].z : xv[i].w;
+          acc[i][0] = ffma2(xq, wl, acc[i][0]);
+          acc[i][1] = ffma2(xq, wh, acc[i][1]);
+        }
+      }
+    }
+    __syncthreads();
+    issue(ck + 2);
+  }
+  // approximate scores -> smem: groups 1..3 park their partial sums (the
+  // x tiles are free now), group 0 adds them: (g0 + g1) + (g2 + g3), two more
+  // roundings per output, inside the bound's split term; |x|^2 -> nrm
+  // (both over the x / fp32-x / W tiles, which are dead after the loop)
+  float* part = reinterpret_cast<float*>(sm);                     // [3][SC_TOK][NCP + 1]
+  float* sc = part + 3 * SC_TOK * (NCP + 1);                      // [SC_TOK][NCP + 1]
+  static_assert(4 * SC_TOK * (NCP + 1) * 4 <= S::X + S::XF + S::W, "partials fit over the tiles");
+  if (grp > 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float* o = part + ((grp - 1) * SC_TOK + ty + 16 * i) * (NCP + 1) + 4 * tx;
+      o[0] = acc[i][0].x;
+      o[1] = acc[i][0].y;
+      o[2] = acc[i][1].x;
+      o[3] = acc[i][1].y;
+    }
+  }
+  if (tid < 4 * SC_TOK) nrm[tid] = nacc;
+  __syncthreads();
+  if (grp == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = ty + 16 * i;
+      const float* p1 = part + r * (NCP + 1) + 4 * tx;
+      const float* p2 = p1 + SC_TOK * (NCP + 1);
+      const float* p3 = p2 + SC_TOK * (NCP + 1);
+      float* o = sc + r * (NCP + 1) + 4 * tx;
+      o[0] = (acc[i][0].x + p1[0]) + (p2[0] + p3[0]);
+      o[1] = (acc[i][0].y + p1[1]) + (p2[1] + p3[1]);
+      o[2] = (acc[i][1].x + p1[2]) + (p2[2] + p3[2]);
+      o[3] = (acc[i][1].y + p1[3]) + (p2[3] + p3[3]);
+    }
+  }
+  __syncthreads();
+  // bounds: |s~ - s_ref| <= cB |x|_2 |w_e|_2 (see the header); |x|^2 summed in
+  // fp32 from exact bf16 squares: s <= s~ (1 + 2 gam), gam = gamma_M
+  for (int pi = tid; pi < ntok * E; pi += NT) {
+    const int tl = pi / E, e = pi % E;
+    const long long o = static_cast<long long>(t0 + tl) * E + e;
+    const double xs2 = (static_cast<double>(nrm[4 * tl]) + static_cast<double>(nrm[4 * tl + 1])) +
+                       (static_cast<double>(nrm[4 * tl + 2]) + static_cast<double>(nrm[4 * tl + 3]));
+    const double xnorm = sqrt(xs2 * (1.0 + 2.0 * gam)) * (1.0 + 1e-12);
+    const float r = sc[tl * (NCP + 1) + e];
+    const double br = cB * xnorm * wn[e];
+    double s, bnd;
+    if (KIND == 0) {
+      const float sp = sc[tl * (NCP + 1) + E + e];
+      const uint64_t o0 = draws[tl * 2 * E_MAX + 2 * e];
+      const uint64_t o1 = draws[tl * 2 * E_MAX + 2 * e + 1];
+      const double u1 = __dmul_rn(__dadd_rn(static_cast<double>(o0 >> 11), 0.5), 0x1.0p-53);
+      const double u2 = __dmul_rn(__dadd_rn(static_cast<double>(o1 >> 11), 0.5), 0x1.0p-53);
+      const double two_pi = 2.0 * 3.141592653589793238462643383279502884;
+      const double n = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
+      const double bs = cB * xnorm * wn[E + e];
+      const double soft = log1p(exp(static_cast<double>(sp)));
+      s = static_cast<double>(r) + n * soft;
+      bnd = br + fabs(n) * bs + 1e-12 * (fabs(static_cast<double>(r)) + fabs(n * soft)) + 1e-300;
+      noise_ws[o] = n;
+      if (spread_out) spread_out[o] = sp;
+    } else {
+      s = r;
+      bnd = br + 1e-12 * fabs(static_cast<double>(r)) + 1e-300;
+    }
+    if (scores_out) scores_out[o] = s;
+    lo[tl * E_MAX + e] = s - bnd;
+    hi[tl * E_MAX + e] = s + bnd;
+  }
+  __syncthreads();
+  // candidates: upper bound reaches the k-th largest lower bound
+  if (tid < ntok) {
+    const double* l = lo + tid * E_MAX;
+    const double* h = hi + tid * E_MAX;
+    uint64_t taken = 0;
+    double kth = 0.0;
+    for (int j = 0; j < k; ++j) {
+      int bi = -1;
+      for (int e = 0; e < E; ++e)
+        if (!((taken >> e) & 1ULL) && (bi < 0 || l[e] > l[bi])) bi = e;
+      taken |= 1ULL << bi;
+      kth = l[bi];
+    }
+    uint64_t m = 0;
+    for (int e = 0; e < E; ++e)
+      if (h[e] >= kth) m |= 1ULL << e;
+    mask[t0 + tid] = m;
+  }
+}
+
+constexpr int XF_TOK = 64;       // tokens per exact/final block
+constexpr int XF_THREADS = 256;
+constexpr int XF_JC = 64;        // columns per stage
+constexpr int XF_XROW = XF_JC * 2 + 16;  // bf16 row bytes (+16: conflict-free LDS.128)
+constexpr int XF_WROW = XF_JC + 2;       // fp64 per W^T smem row (+16 B, same reason)
+
+template <int NPROJ, int E_MAX>
+struct XfSmem {
+  static constexpr int XS = XF_TOK * XF_XROW;             // token rows of one stage
+  static constexpr int WS = NPROJ * E_MAX * XF_WROW * 8;   // W^T rows (fp64) of one stage
+  static constexpr int STAGE = XS + WS;
+  static constexpr int BYTES = 2 * STAGE;
+};
+
+// Exact fp64 logits of each token's candidates (the reference's sequential
+// separately rounded mul/add over j, workload.cpp:103-108) with the token
+// rows and all W^T rows streamed through shared memory in XF_JC-column
+// stages (cp.async, double-buffered); thread = (token, candidate, projection).
+// Then the final exact top-k, weights and picks for the block's tokens.
+template <int KIND, int E_MAX>
+__global__ void __launch_bounds__(XF_THREADS)
+    exact_final_kernel(const __nv_bfloat16* __restrict__ x, int T, int M, int E, int k,
+                       const double* __restrict__ WT, const uint64_t* __restrict__ mask,
+                       const double* __restrict__ noise, int* __restrict__ pick_token,
+                       int* __restrict__ pick_expert, double* __restrict__ pick_weight,
+                       double* __restrict__ scores_out, double* __restrict__ spread_out) {
+  constexpr int NPROJ = KIND == 0 ? 2 : 1;
+  using S = XfSmem<NPROJ, E_MAX>;
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint64_t msk[XF_TOK];
+  __shared__ int cnt[XF_TOK];
+  __shared__ short2 items[XF_TOK * E_MAX];
+  __shared__ int nitems;
+  __shared__ double ex[NPROJ][XF_TOK][E_MAX];
+  const int tid = threadIdx.x;
+  const int t0 = blockIdx.x * XF_TOK;
+  const int ntok = min(XF_TOK, T - t0);
+  const int nW = NPROJ * E;
+  auto issue = [&](int ck) {
+    if (ck * XF_JC < M) {
+      uint8_t* st = sm + (ck & 1) * S::STAGE;
+      const int j0 = ck * XF_JC;
+      for (int i = tid; i < XF_TOK * (XF_JC / 8); i += XF_THREADS) {
+        const int r = i / (XF_JC / 8), c = i % (XF_JC / 8);
+        const int t = t0 + (r < ntok ? r : 0);
+        cp_async16(st + r * XF_XROW + c * 16, x + static_cast<long long>(t) * M + j0 + c * 8);
+      }
+      double* ws = reinterpret_cast<double*>(st + S::XS);
+      for (int i = tid; i < nW * (XF_JC / 2); i += XF_THREADS) {
+        const int r = i / (XF_JC / 2), c = i % (XF_JC / 2);
+        cp_async16(ws + r * XF_WROW + c * 2, WT + static_cast<long long>(r) * M + j0 + c * 2);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  if (tid < XF_TOK) {
+    const uint64_t m = tid < ntok ? mask[t0 + tid] : 0ULL;
+    msk[tid] = m;
+    cnt[tid] = __popcll(m);
+  }
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of the 64 counts by one warp
+    const int c0 = cnt[tid], c1 = cnt[tid + 32];
+    int a0 = c0, a1 = c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v0 = __shfl_up_sync(0xffffffffu, a0, o), v1 = __shfl_up_sync(0xffffffffu, a1, o);
+      if (tid >= o) { a0 += v0; a1 += v1; }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, a0, 31);
+    int w0 = a0 - c0, w1 = tot0 + a1 - c1;
+    for (uint64_t mm = msk[tid]; mm; mm &= mm - 1)
+      items[w0++] = make_short2(static_cast<short>(tid), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
+    for (uint64_t mm = msk[tid + 32]; mm; mm &= mm - 1)
+      items[w1++] = make_short2(static_cast<short>(tid + 32), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
+    if (tid == 31) nitems = tot0 + a1;
+  }
+  __syncthreads();
+  const int nc = nitems;
+  const int nwork = nc * NPROJ;
+  // work item = (projection, candidate), projection-major so that the lanes of
+  // a warp read rows of one projection (padded rows: conflict-free); a thread
+  // holds up to 2 dot products (a block rarely has > 256 items)
+  double acc0 = 0.0, acc1 = 0.0;
+  const int it0 = tid, it1 = tid + XF_THREADS;
+  short2 te0 = make_short2(0, 0), te1 = make_short2(0, 0);
+  int pj0 = 0, pj1 = 0;
+  if (it0 < nwork) { te0 = items[it0 % nc]; pj0 = it0 / nc; }
+  if (it1 < nwork) { te1 = items[it1 % nc]; pj1 = it1 / nc; }
+  const int nck = (M + XF_JC - 1) / XF_JC;
+  for (int ck = 0; ck < nck; ++ck) {
+    if (ck + 1 < nck) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    const uint8_t* st = sm + (ck & 1) * S::STAGE;
+    const double* ws = reinterpret_cast<const double*>(st + S::XS);
+    auto run = [&](double& acc, short2 te, int pj) {
+      const uint8_t* xr = st + te.x * XF_XROW;
+      const double* wr = ws + (pj * E + te.y) * XF_WROW;
+#pragma unroll 4
+      for (int j = 0; j < XF_JC; j += 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(xr + 2 * j);
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 wv = *reinterpret_cast<const double2*>(wr + j + 2 * q);
+          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] << 16)), wv.x));
+          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] & 0xffff0000u)), wv.y));
+        }
+      }
+    };
+    if (it0 < nwork) run(acc0, te0, pj0);
+    if (it1 < nwork) run(acc1, te1, pj1);
+    __syncthreads();
+    issue(ck + 2);
+  }
+  if (it0 < nwork) ex[pj0][te0.x][te0.y] = acc0;
+  if (it1 < nwork) ex[pj1][te1.x][te1.y] = acc1;
+  // more than 2 * XF_THREADS dot products: the rest from global memory
+  for (int it = it1 + XF_THREADS; it < nwork; it += XF_THREADS) {
+    const short2 te = items[it % nc];
+    const int pj = it / nc;
+    const __nv_bfloat16* xr = x + static_cast<long long>(t0 + te.x) * M;
+    const double* wr = WT + static_cast<long long>(pj * E + te.y) * M;
+    double acc = 0.0;
+    for (int j = 0; j < M; ++j)
+      acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__bfloat162float(xr[j])), wr[j]));
+    ex[pj][te.x][te.y] = acc;
+  }
+  __syncthreads();
+  if (tid >= ntok) return;
+  const int t = t0 + tid;
+  const uint64_t cand = msk[tid];
+  const long long row = static_cast<long long>(t) * E;
+  double* s = ex[0][tid];
+  for (uint64_t m = cand; m; m &= m - 1) {
+    const int e = __ffsll(static_cast<long long>(m)) - 1;
+    if (KIND == 0) {  // s = raw + n * softplus(spread)   (workload.cpp:186)
+      s[e] = __dadd_rn(s[e], __dmul_rn(noise[row + e], log1p(exp(ex[NPROJ - 1][tid][e]))));
+      if (spread_out) spread_out[row + e] = ex[NPROJ - 1][tid][e];
+    }
+    if (scores_out) scores_out[row + e] = s[e];
+  }
+  uint64_t kept = 0;
+  for (int j = 0; j < k; ++j) {
+    int bi = -1;
+    double best = 0.0;
+    for (uint64_t m = cand & ~kept; m; m &= m - 1) {
+      const int e = __ffsll(static_cast<long long>(m)) - 1;
+      if (bi < 0 || s[e] > best) {
+        best = s[e];
+        bi = e;
+      }
+    }
+    kept |= 1ULL << bi;
+  }
+  const long long pb = static_cast<long long>(t) * k;
+  if (KIND == 1) {
+    uint64_t m = kept;
+    for (int j = 0; j < k; ++j) {
+      const int e = __ffsll(static_cast<long long>(m)) - 1;
+      m &= m - 1;
+      pick_token[pb + j] = t;
+      pick_expert[pb + j] = e;
+      pick_weight[pb + j] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-s[e])));
+    }
+  } else {
+    uint64_t m = kept;
+    double mx = s[__ffsll(static_cast<long long>(m)) - 1];
+    for (; m; m &= m - 1) {
+      const double v = s[__ffsll(static_cast<long long>(m)) - 1];
+      mx = (mx < v) ? v : mx;
+    }
+    double z = 0.0;
+    for (m = kept; m; m &= m - 1) z = __dadd_rn(z, exp(__dsub_rn(s[__ffsll(static_cast<long long>(m)) - 1], mx)));
+    m = kept;
+    for (int j = 0; j < k; ++j) {
+      const int e = __ffsll(static_cast<long long>(m)) - 1;
+      m &= m - 1;
+      pick_token[pb + j] = t;
+      pick_expert[pb + j] = e;
+      pick_weight[pb + j] = __ddiv_rn(exp(__dsub_rn(s[e], mx)), z);
+    }
+  }
+}
+
+template <int KIND, int NCP, int E_MAX>
+void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const float* W32,
+                  const double* WT, const double* wn, double* noise_ws, uint64_t* mask,
+                  int* pick_token, int* pick_expert, double* pick_weight, double* scores_out,
+                  double* spread_out, cudaStream_t st) {
+  const int T = d.tokens, M = d.model_dim, E = d.score_cols, k = d.top_k;
+  const int NC = KIND == 0 ? 2 * E : E;
+  const double u = 0x1.0p-24;
+  const double gam = M * u / (1.0 - M * u);
+  constexpr int SMEM = ScreenSmem<NCP, E_MAX>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(screen_kernel<KIND, NCP, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const auto* xb = static_cast<const __nv_bfloat16*>(x);
+  screen_kernel<KIND, NCP, E_MAX><<<(T + SC_TOK - 1) / SC_TOK, NCP * 4 * SC_GRP, SMEM, st>>>(
+      xb, T, M, E, k, W32, NC, wn, cB, gam, d.seed, noise_ws, scores_out, spread_out, mask);
+  ::fsmoe::count_launch();
+  constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
+  static bool xattr = false;
+  if (!xattr) {
+    cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM);
+    xattr = true;
+  }
+  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, XSMEM, st>>>(
+      xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
+      spread_out);
+  ::fsmoe::count_launch();
+}
+
 struct PruneWs {
   float* W32;
   double* WT;
@@ -587,6 +1069,32 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
   FSMOE_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int) * E, st), "gate memset");
   w_prep_kernel<<<NC, 256, 0, st>>>(M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn);
   ::fsmoe::count_launch();
+  const bool fused = d.x_dtype == FSMOE_BF16 && E <= 32 && NC % 4 == 0 && M % SC_JC == 0 &&
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0 && !getenv("FSMOE_GATE_UNFUSED");
+  if (fused) {
+    // the fused screen sums each token's FMA chain without splits: the same
+    // bound with the split term kept (conservative)
+    const double cBf = (M + AP_KS + 4.0) * 0x1.0p-24 * 1.01 + (M + 2.0) * 0x1.0p-53;
+    double* nz = noise_out ? noise_out : w.noise;
+    if (noisy) {
+      if (E <= 16) launch_fused<0, 32, 16>(d, x, cBf, w.W32, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+      else launch_fused<0, 64, 32>(d, x, cBf, w.W32, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+    } else {
+      launch_fused<1, 32, 32>(d, x, cBf, w.W32, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+    }
+    if (getenv("FSMOE_GATE_DEBUG")) {  // candidate statistics (synchronises)
+      std::vector<uint64_t> hm(static_cast<size_t>(T));
+      cudaMemcpyAsync(hm.data(), w.mask, 8ull * T, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      long long tot = 0, mx = 0;
+      for (uint64_t m : hm) {
+        tot += __builtin_popcountll(m);
+        mx = std::max<long long>(mx, __builtin_popcountll(m));
+      }
+      fprintf(stderr, "fsmoe gate: %lld candidates for %d tokens (max %lld per token)\n", tot, T, mx);
+    }
+    return cuda_status(cudaGetLastError(), "fsmoe_gate(fused)");
+  }
   dim3 grid((T + AP_TOK - 1) / AP_TOK, (NC + AP_COL - 1) / AP_COL, AP_KS);
   switch (d.x_dtype) {
     case FSMOE_F64: approx_scores_kernel<0><<<grid, 64, 0, st>>>(x, T, M, w.W32, NC, w.part, w.xn2); break;

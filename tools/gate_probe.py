@@ -15,11 +15,13 @@ def run(T=16384, M=1024, E=16, k=1, kind="noisy_topk", reps=5):
     ws = ((torch.rand(M, E, device="cuda", generator=g, dtype=torch.float64) * 2 - 1) / M ** 0.5)
     wn = ((torch.rand(M, E, device="cuda", generator=g, dtype=torch.float64) * 2 - 1) / M ** 0.5)
     out = {}
-    for path in ("pruned", "exhaustive"):
+    for path in ("pruned", "unfused", "exhaustive"):
+        os.environ.pop("FSMOE_GATE_EXHAUSTIVE", None)
+        os.environ.pop("FSMOE_GATE_UNFUSED", None)
         if path == "exhaustive":
             os.environ["FSMOE_GATE_EXHAUSTIVE"] = "1"
-        else:
-            os.environ.pop("FSMOE_GATE_EXHAUSTIVE", None)
+        if path == "unfused":
+            os.environ["FSMOE_GATE_UNFUSED"] = "1"
         r = ops.gate(kind, k, 7, x, ws, wn, save=True)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,9 +32,14 @@ def run(T=16384, M=1024, E=16, k=1, kind="noisy_topk", reps=5):
         torch.cuda.synchronize()
         out[path] = (s.elapsed_time(e) / reps * 1e3, r)
         print(f"{path}: {out[path][0]:.1f} us per gate call")
-    a, b = out["pruned"][1], out["exhaustive"][1]
-    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
-    print("identical picks; max weight diff", (a[2] - b[2]).abs().max().item())
+    a = out["pruned"][1]
+    for other in ("unfused", "exhaustive"):
+        b = out[other][1]
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        print(f"pruned vs {other}: identical picks; max weight diff",
+              (a[2] - b[2]).abs().max().item())
+        for key in a[3]:
+            print(f"  saved {key}: max diff", (a[3][key] - b[3][key]).abs().max().item())
 
 
 if __name__ == "__main__":
