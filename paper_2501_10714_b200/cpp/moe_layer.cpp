@@ -146,6 +146,10 @@ struct MoELayer::Impl {
   std::vector<Chunk> fwd_chunks, bwd_chunks;
 
   cudaStream_t s_comp = nullptr, s_comm = nullptr;
+  // second compute stream: the backward's wgrad GEMMs run beside the dgrad
+  // GEMMs they do not depend on, so each fills the other's last wave
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_x1 = nullptr, ev_x2 = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_gate = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_a, ev_b;  // per-chunk (max of r_fwd, r_bwd)
 
@@ -257,16 +261,20 @@ struct MoELayer::Impl {
     for (void* p : owned) cudaFree(p);
     for (auto e : ev_a) cudaEventDestroy(e);
     for (auto e : ev_b) cudaEventDestroy(e);
-    for (auto e : {ev_in, ev_out, ev_gate, ev_join})
+    for (auto e : {ev_in, ev_out, ev_gate, ev_join, ev_x1, ev_x2})
       if (e) cudaEventDestroy(e);
+    if (s_aux) {
+      cudaStreamSynchronize(s_aux);
+      cudaStreamDestroy(s_aux);
+    }
     if (s_comp) cudaStreamDestroy(s_comp);
     if (s_comm) cudaStreamDestroy(s_comm);
   }
 
   // ------------------------------------------------------------- GEMMs --
-  void gemm(fsmoe_gemm_desc& d) {
+  void gemm(fsmoe_gemm_desc& d, cudaStream_t st = nullptr) {
     d.precision = cfg.precision == Precision::f32 ? 1 : 0;
-    throw_on(fsmoe_grouped_gemm(&d, s_comp));
+    throw_on(fsmoe_grouped_gemm(&d, st ? st : s_comp));
   }
 
   fsmoe_gemm_desc row_desc(const Chunk& c) const {
@@ -328,6 +336,13 @@ struct MoELayer::Impl {
   void expert_bwd(const Chunk& c, bool first) {
     const bool bf = cfg.precision == Precision::bf16;
     const bool gated = cfg.ffn == LayerConfig::Ffn::gated3;
+    // bf16: wgrad GEMMs on s_aux beside the dgrad GEMMs (independent inputs and
+    // outputs); fp32 check mode writes dH over H, which wgrad2 reads: serial
+    cudaStream_t sw = bf ? s_aux : s_comp;
+    if (bf) {
+      record(ev_x1, s_comp);
+      wait(s_aux, ev_x1);
+    }
     // wgrad2: dW2[e] (M x H) += dO^T H
     fsmoe_gemm_desc w2 = k_desc(c, !first);
     w2.Mo = M;
@@ -336,7 +351,7 @@ struct MoELayer::Impl {
     w2.B = Hh;
     w2.D = prm.g_w2;
     w2.ldd = H;
-    gemm(w2);
+    gemm(w2, sw);
     // dgrad2: dH = dO W2 ; dZ = dH * act'(Z)   (written over Z)
     fsmoe_gemm_desc d2 = row_desc(c);
     d2.K = M;
@@ -360,6 +375,11 @@ struct MoELayer::Impl {
                                     static_cast<const float*>(Hh), static_cast<const float*>(Z),
                                     static_cast<float*>(Z), s_comp));
     }
+    // wgrad1 needs dZ: after dgrad2 (and after wgrad2 in stream order on sw)
+    if (bf) {
+      record(ev_x1, s_comp);
+      wait(s_aux, ev_x1);
+    }
     // wgrad1: dW1[e] (N1 x M) += dZ^T X
     fsmoe_gemm_desc w1 = k_desc(c, !first);
     w1.Mo = N1;
@@ -368,7 +388,7 @@ struct MoELayer::Impl {
     w1.B = Xr;
     w1.D = prm.g_w1;
     w1.ldd = M;
-    gemm(w1);
+    gemm(w1, sw);
     // dgrad1: dX = dZ W1
     fsmoe_gemm_desc d1 = row_desc(c);
     d1.K = N1;
@@ -381,6 +401,11 @@ struct MoELayer::Impl {
     d1.epi = bf ? 0 : 1;
     if (peer) d1.d_peers = &map_dX;  // backward combine fused into the epilogue
     gemm(d1);
+    if (bf) {
+      // rejoin: the next chunk's dgrad2 overwrites Z, which wgrad1 reads
+      record(ev_x2, s_aux);
+      wait(s_comp, ev_x2);
+    }
   }
 
   // ------------------------------------------------------- exchanges --
@@ -501,7 +526,8 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   cuda_check(cudaStreamCreateWithPriority(&I.s_comm, cudaStreamNonBlocking, hi), "stream");
-  for (cudaEvent_t* e : {&I.ev_in, &I.ev_out, &I.ev_gate, &I.ev_join})
+  cuda_check(cudaStreamCreateWithPriority(&I.s_aux, cudaStreamNonBlocking, 0), "stream");
+  for (cudaEvent_t* e : {&I.ev_in, &I.ev_out, &I.ev_gate, &I.ev_join, &I.ev_x1, &I.ev_x2})
     cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
   const size_t nev = std::max(I.fwd_chunks.size(), I.bwd_chunks.size());
   I.ev_a.resize(nev);

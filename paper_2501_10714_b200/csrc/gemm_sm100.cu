@@ -30,11 +30,10 @@ namespace {
 using namespace fsmoe_dev;
 
 constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BN_MAX = 256;  // tile columns: 256, or 128 when 256 leaves a ragged last wave
 constexpr int BK = 64;
 constexpr int NUM_THREADS = 384;
 constexpr int EPI_THREADS = 256;  // 8 epilogue warps
-constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
 
 struct KParams {
   int kind;  // GemmKind
@@ -115,6 +114,44 @@ __device__ __forceinline__ void gelu_and_grad(float z, float& h, float& g) {
   h = z * cdf;
   g = fmaf(z * 0.39894228040143268f, e, cdf);
 }
+// Packed fp32 pairs (FFMA2 / FMUL2 / FADD2, sm_100): two IEEE operations per
+// instruction, which halves the epilogue's FP32 issue count.
+__device__ __forceinline__ unsigned long long f2u(float2 v) {
+  return *reinterpret_cast<unsigned long long*>(&v);
+}
+__device__ __forceinline__ float2 u2f(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+
+// gelu_and_grad on a pair of values (same formula, paired arithmetic)
+__device__ __forceinline__ void gelu_and_grad2(float2 z, float2& h, float2& g) {
+  const float2 x = mul2(make_float2(fabsf(z.x), fabsf(z.y)), bc2(0.70710678118654752f));
+  const float2 den = fma2(bc2(0.3275911f), x, bc2(1.0f));
+  const float2 t = make_float2(__fdividef(1.0f, den.x), __fdividef(1.0f, den.y));
+  float2 poly = fma2(bc2(1.061405429f), t, bc2(-1.453152027f));
+  poly = fma2(poly, t, bc2(1.421413741f));
+  poly = fma2(poly, t, bc2(-0.284496736f));
+  poly = fma2(poly, t, bc2(0.254829592f));
+  poly = mul2(poly, t);
+  const float2 q = mul2(mul2(z, z), bc2(-0.5f * 1.4426950408889634f));
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(q.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(q.y));
+  const float2 tail = mul2(mul2(poly, e), bc2(0.5f));  // 0.5 (1 - erf(x))
+  const float2 cdf = make_float2(z.x >= 0.f ? 1.0f - tail.x : tail.x, z.y >= 0.f ? 1.0f - tail.y : tail.y);
+  h = mul2(z, cdf);
+  g = fma2(mul2(z, bc2(0.39894228040143268f)), e, cdf);
+}
+
 __device__ __forceinline__ float sigmoid_f(float z) { return 1.0f / (1.0f + __expf(-z)); }
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
@@ -147,17 +184,22 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
 // CTAS = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
 // with cta_group::2: each CTA stages its 128 rows of A and 128 of the 256
 // B rows; the leader issues the MMAs and both TMEMs hold their 128 rows.
-template <int CTAS>
+template <int CTAS, int BN_ = BN_MAX>
 struct TileCfg {
   static constexpr int BM = 128 * CTAS;      // tile rows (whole pair)
+  static constexpr int BN = BN_;             // tile columns
   static constexpr int BN_CTA = BN / CTAS;   // B rows staged per CTA
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NSTAGE = CTAS == 1 ? 3 : 5;
-  static constexpr int STG_OFF = NSTAGE * STAGE + 1024;         // after the barrier block
   static constexpr int STG_PER_WARP = 8192;                     // two 4 KB SW128 boxes
-  static constexpr int SMEM = STG_OFF + (EPI_THREADS / 32) * STG_PER_WARP + 1024;
+  static constexpr int STG_TOTAL = (EPI_THREADS / 32) * STG_PER_WARP;
+  // as many stages as fit next to the epilogue boxes (<= 6)
+  static constexpr int NS_FIT = (227 * 1024 - 2048 - STG_TOTAL) / STAGE;
+  static constexpr int NSTAGE = NS_FIT > 6 ? 6 : NS_FIT;
+  static constexpr int STG_OFF = NSTAGE * STAGE + 1024;         // after the barrier block
+  static constexpr int SMEM = STG_OFF + STG_TOTAL + 1024;
+  static constexpr int TMEM_COLS = 2 * BN;                      // double-buffered accumulator
 };
 
 // Epilogue tensor maps (TMA stores / loads of 32-row x 128-byte SW128 boxes):
@@ -180,13 +222,15 @@ __device__ __forceinline__ TileInfo decode_tile_c(const KParams& p, int t) {
   return ti;
 }
 
-template <int CTAS>
+template <int CTAS, int BN_>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const KParams p,
                         const __grid_constant__ EpiMaps em) {
-  using Cfg = TileCfg<CTAS>;
+  using Cfg = TileCfg<CTAS, BN_>;
   constexpr int NS = Cfg::NSTAGE;
+  constexpr int BN = BN_;
+  constexpr int CPH = BN / 64;  // 32-column TMEM chunks per epilogue warp (half the tile)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -220,8 +264,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) {
-    if constexpr (CTAS == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
-    else tmem_alloc<TMEM_COLS>(tmem_slot);
+    if constexpr (CTAS == 2) tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
+    else tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   }
   tc_fence_before();
   if constexpr (CTAS == 2) cluster_sync();
@@ -376,8 +420,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
           bulk_wait_read<0>();  // the previous tile's stores have left the boxes
 #pragma unroll
-          for (int pc = 0; pc < 2; ++pc) {
-            const int col = ti.nt * BN + (4 * half + 2 * pc) * 32;
+          for (int pc = 0; pc < CPH / 2; ++pc) {
+            const int col = ti.nt * BN + (CPH * half + 2 * pc) * 32;
             if (col < p.out_cols) {
               mbar_arrive_expect_tx(&zb[pc], 4096);
               tma_load_3d(stg + pc * 4096, &em.z, &zb[pc], col, c1, ti.g);
@@ -398,7 +442,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float v[32];
       if (tma_epi && p.epi == static_cast<int>(Epi::StoreF32)) {
         // fp32: one 32-column TMEM chunk = one box
-        for (int c = 4 * half; c < 4 * half + 4; ++c) {
+        for (int c = CPH * half; c < CPH * half + CPH; ++c) {
           const int col = ti.nt * BN + c * 32;
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
@@ -424,8 +468,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       } else if (tma_epi) {
         // bf16: two TMEM chunks (64 columns) = one box
-        for (int pc = 0; pc < 2; ++pc) {
-          const int c = 4 * half + 2 * pc;
+        for (int pc = 0; pc < CPH / 2; ++pc) {
+          const int c = CPH * half + 2 * pc;
           const int col = ti.nt * BN + c * 32;
           if (col >= p.out_cols) continue;  // warp-uniform
           uint32_t r2[32];
@@ -465,11 +509,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint4* bh = box_row(stg + 4096);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-              float h[8], g[8];
+              uint32_t hp[4], gp[4];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) gelu_and_grad(bf2f(__float2bfloat16(val(8 * k + j))), h[j], g[j]);
-              bg[k ^ sw] = make_uint4(pk(g[0], g[1]), pk(g[2], g[3]), pk(g[4], g[5]), pk(g[6], g[7]));
-              bh[k ^ sw] = make_uint4(pk(h[0], h[1]), pk(h[2], h[3]), pk(h[4], h[5]), pk(h[6], h[7]));
+              for (int j = 0; j < 4; ++j) {
+                // the bf16-rounded Z (what the backward sees) as a pair
+                __nv_bfloat162 zb = __floats2bfloat162_rn(val(8 * k + 2 * j), val(8 * k + 2 * j + 1));
+                float2 h2, g2;
+                gelu_and_grad2(__bfloat1622float2(zb), h2, g2);
+                hp[j] = pk(h2.x, h2.y);
+                gp[j] = pk(g2.x, g2.y);
+              }
+              bg[k ^ sw] = make_uint4(gp[0], gp[1], gp[2], gp[3]);
+              bh[k ^ sw] = make_uint4(hp[0], hp[1], hp[2], hp[3]);
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -539,7 +590,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {  // SwigluBwd: acc = dH over H units; dZ at the interleaved gate/up columns
         const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
         __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-        for (int c = 4 * half; c < 4 * half + 4; ++c) {
+        for (int c = CPH * half; c < CPH * half + CPH; ++c) {
           const int col = ti.nt * BN + c * 32;
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
@@ -584,8 +635,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    if constexpr (CTAS == 2) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
-    else tmem_dealloc<TMEM_COLS>(tmem_base);
+    if constexpr (CTAS == 2) tmem_dealloc_pair<Cfg::TMEM_COLS>(tmem_base);
+    else tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -685,9 +736,17 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   const int units_cols = pr.kind == GemmKind::RowGrouped ? pr.N : pr.No;
   const int groups = pr.kind == GemmKind::RowGrouped ? pr.nblk : p.n_w;
   long long pair_tiles = static_cast<long long>(groups) * ((units_rows + 255) / 256) *
-                         ((units_cols + BN - 1) / BN);
+                         ((units_cols + BN_MAX - 1) / BN_MAX);
   int ctas = pair_tiles >= num_sms() / 4 ? 2 : 1;
   if (const char* env = getenv("FSMOE_GEMM_CTAS")) ctas = atoi(env) == 1 ? 1 : 2;
+  // Tile width: 256 columns. 128-column tiles (FSMOE_GEMM_BN=128) fill a
+  // ragged last wave better (N = 1024 over 74 SM pairs: 3.46 -> 6.92 waves)
+  // but measured slower on B200 (fwd2 109 -> 130 us: each MMA re-reads A for
+  // half the columns); the layer instead overlaps independent GEMMs on two
+  // streams so one fills the other's tail. SwiGLU needs the 256-column tile.
+  int BN = BN_MAX;
+  if (const char* env = getenv("FSMOE_GEMM_BN"))
+    if (pr.epi != Epi::SwigluFwd && pr.epi != Epi::SwigluBwd) BN = atoi(env) == 128 ? 128 : 256;
   const int bm = 128 * ctas, bn_cta = BN / ctas;
   if (pr.kind == GemmKind::RowGrouped) {
     if (pr.K % 8 || pr.N % 64 || pr.K <= 0 || pr.N <= 0) return cudaErrorInvalidValue;
@@ -751,34 +810,37 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
       }
     }
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(grouped_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TileCfg<1>::SMEM);
-    cudaFuncSetAttribute(grouped_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TileCfg<2>::SMEM);
-    attr_set = true;
-  }
   const int max_units = num_sms() / ctas;
   const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
-  if (ctas == 1) {
-    grouped_gemm_kernel<1><<<units, NUM_THREADS, TileCfg<1>::SMEM, stream>>>(ta, tb, p, em);
-  } else {
+  static bool smem_set[2][2] = {{false, false}, {false, false}};
+  auto launch = [&](auto kern, int smem) -> cudaError_t {
+    bool& done = smem_set[ctas - 1][BN == 256 ? 1 : 0];
+    if (!done) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      done = true;
+    }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(units * 2);
+    cfg.gridDim = dim3(units * ctas);
     cfg.blockDim = dim3(NUM_THREADS);
-    cfg.dynamicSmemBytes = TileCfg<2>::SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = ctas;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<2>, ta, tb, p, em);
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
+    cfg.numAttrs = ctas == 2 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, ta, tb, p, em);
+  };
+  cudaError_t e;
+  if (ctas == 1)
+    e = BN == 256 ? launch(grouped_gemm_kernel<1, 256>, TileCfg<1, 256>::SMEM)
+                  : launch(grouped_gemm_kernel<1, 128>, TileCfg<1, 128>::SMEM);
+  else
+    e = BN == 256 ? launch(grouped_gemm_kernel<2, 256>, TileCfg<2, 256>::SMEM)
+                  : launch(grouped_gemm_kernel<2, 128>, TileCfg<2, 128>::SMEM);
+  if (e != cudaSuccess) return static_cast<int>(e);
   ::fsmoe::count_launch();
   return static_cast<int>(cudaGetLastError());
 }

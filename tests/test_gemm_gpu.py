@@ -19,12 +19,15 @@ def _ops():
     return ops
 
 
-@pytest.fixture(params=["1", "2"], autouse=True)
+@pytest.fixture(params=["1x256", "2x256", "1x128", "2x128"], autouse=True)
 def gemm_ctas(request, monkeypatch):
-    """Run every GEMM test on both tile variants: single-CTA 128x256 and the
-    CTA-pair 256x256 (tcgen05 cta_group::2)."""
-    monkeypatch.setenv("FSMOE_GEMM_CTAS", request.param)
-    return request.param
+    """Run every GEMM test on all tile variants: single-CTA (128 rows) and
+    CTA-pair (256 rows, tcgen05 cta_group::2) x 256- and 128-column tiles
+    (SwiGLU epilogues always take 256 columns)."""
+    ctas, bn = request.param.split("x")
+    monkeypatch.setenv("FSMOE_GEMM_CTAS", ctas)
+    monkeypatch.setenv("FSMOE_GEMM_BN", bn)
+    return ctas
 
 
 def _rel(a, b):
