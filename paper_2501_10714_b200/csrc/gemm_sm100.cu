@@ -132,22 +132,39 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
 
-// gelu_and_grad on a pair of values (same formula, paired arithmetic)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// gelu_and_grad on a pair of values, same formula in paired arithmetic with
+// the branch-free Phi(z) = 0.5 + sign(z) (0.5 - tail), tail = 0.5 poly(t) e
+// (the 0.5 folded into the coefficients): ~13 instructions per value.
 __device__ __forceinline__ void gelu_and_grad2(float2 z, float2& h, float2& g) {
-  const float2 x = mul2(make_float2(fabsf(z.x), fabsf(z.y)), bc2(0.70710678118654752f));
-  const float2 den = fma2(bc2(0.3275911f), x, bc2(1.0f));
-  const float2 t = make_float2(__fdividef(1.0f, den.x), __fdividef(1.0f, den.y));
-  float2 poly = fma2(bc2(1.061405429f), t, bc2(-1.453152027f));
-  poly = fma2(poly, t, bc2(1.421413741f));
-  poly = fma2(poly, t, bc2(-0.284496736f));
-  poly = fma2(poly, t, bc2(0.254829592f));
+  const float2 az = make_float2(fabsf(z.x), fabsf(z.y));
+  const float2 den = fma2(az, bc2(0.3275911f * 0.70710678118654752f), bc2(1.0f));
+  const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+  float2 poly = fma2(bc2(0.5f * 1.061405429f), t, bc2(0.5f * -1.453152027f));
+  poly = fma2(poly, t, bc2(0.5f * 1.421413741f));
+  poly = fma2(poly, t, bc2(0.5f * -0.284496736f));
+  poly = fma2(poly, t, bc2(0.5f * 0.254829592f));
   poly = mul2(poly, t);
-  const float2 q = mul2(mul2(z, z), bc2(-0.5f * 1.4426950408889634f));
-  float2 e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(q.x));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(q.y));
-  const float2 tail = mul2(mul2(poly, e), bc2(0.5f));  // 0.5 (1 - erf(x))
-  const float2 cdf = make_float2(z.x >= 0.f ? 1.0f - tail.x : tail.x, z.y >= 0.f ? 1.0f - tail.y : tail.y);
+  const float2 q = mul2(mul2(z, bc2(-0.5f * 1.4426950408889634f)), z);
+  const float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
+  const float2 u = fma2(mul2(poly, e), bc2(-1.0f), bc2(0.5f));  // 0.5 - tail >= 0
+  const float2 su = make_float2(copysignf(u.x, z.x), copysignf(u.y, z.y));
+  const float2 cdf = add2(su, bc2(0.5f));
   h = mul2(z, cdf);
   g = fma2(mul2(z, bc2(0.39894228040143268f)), e, cdf);
 }
@@ -440,6 +457,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       uint32_t r[32];
       float v[32];
+      // hand the accumulator back to the MMA warp as soon as this warp's last
+      // TMEM read of the tile has landed (the rest works from registers)
+      bool released = false;
+      auto release_acc = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CTAS == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
+        released = true;
+      };
       if (tma_epi && p.epi == static_cast<int>(Epi::StoreF32)) {
         // fp32: one 32-column TMEM chunk = one box
         for (int c = CPH * half; c < CPH * half + CPH; ++c) {
@@ -451,6 +480,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) r[i] = 0u;
           }
+          if (c == CPH * half + CPH - 1) release_acc();
           if (col >= p.out_cols) continue;  // warp-uniform
           uint8_t* box = stg + (c & 1) * 4096;
           if (lane == 0) bulk_wait_read<1>();
@@ -471,7 +501,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int pc = 0; pc < CPH / 2; ++pc) {
           const int c = CPH * half + 2 * pc;
           const int col = ti.nt * BN + c * 32;
-          if (col >= p.out_cols) continue;  // warp-uniform
           uint32_t r2[32];
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
@@ -481,6 +510,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) r[i] = r2[i] = 0u;
           }
+          if (pc == CPH / 2 - 1) release_acc();
+          if (col >= p.out_cols) continue;  // warp-uniform
           auto pk = [&](float a, float b) {
             __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
             return *reinterpret_cast<uint32_t*>(&h);
@@ -618,12 +649,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           store_bf16x32(dZ + gcol + 128, u);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CTAS == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
-        else mbar_arrive(&tempty_bar[acc]);
-      }
+      if (!released) release_acc();
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();  // outputs written before the kernel retires
