@@ -18,10 +18,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
+#include <cstdlib>
 
 #include "capi_common.h"
 #include "kernels.h"
 #include "route_common.cuh"
+#include "sm100.cuh"
 
 namespace fsmoe {
 namespace {
@@ -220,6 +223,54 @@ __global__ void __launch_bounds__(256)
   for (int i = lane; i < row_vecs; i += 32) dst[i] = src[i];
 }
 
+// Row moves through the TMA engine: lane r of the block's warp owns row r,
+// bulk-loads its source row (global -> shared) and bulk-stores it to the
+// destination (local or a peer's buffer over NVLink). One instruction moves a
+// whole row, so the LSU / register path that limits the warp-per-row copy
+// (long-scoreboard + lg_throttle stalls, ncu) drops out.
+constexpr int BK_ROWS = 32;  // rows per block (one warp)
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_src))), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(32)
+    dispatch_bulk_kernel(long long n_slots, int row_bytes, int E, long long C, int chunks,
+                         const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
+                         const uint8_t* __restrict__ x, const PeerRows buf) {
+  extern __shared__ __align__(128) uint8_t sm[];  // [BK_ROWS][row_bytes] + one zero row
+  __shared__ __align__(8) uint64_t bar;
+  const int lane = threadIdx.x;
+  const long long s = blockIdx.x * static_cast<long long>(BK_ROWS) + lane;
+  uint8_t* zero = sm + BK_ROWS * row_bytes;
+  for (int i = lane * 16; i < row_bytes; i += 32 * 16) *reinterpret_cast<uint4*>(zero + i) = make_uint4(0, 0, 0, 0);
+  if (lane == 0) {
+    fsmoe_dev::mbar_init(&bar, 32);
+    fsmoe_dev::fence_barrier_init();
+  }
+  __syncwarp();
+  int p = -1;
+  const bool valid = s < n_slots;
+  if (valid) p = pick_of_slot[s];
+  uint8_t* mine = sm + lane * row_bytes;
+  if (p >= 0) {
+    fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
+    fsmoe_dev::bulk_load(mine, x + static_cast<long long>(ptok[p]) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
+  } else {
+    fsmoe_dev::mbar_arrive(&bar);
+  }
+  fsmoe_dev::fence_proxy_async_smem();  // the zero row (generic writes) -> async proxy
+  fsmoe_dev::mbar_wait(&bar, 0);
+  if (valid) {
+    char* dst = peer_row(buf, slot_row(s, E, C, chunks), row_bytes);
+    bulk_store(dst, p >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
+    fsmoe_dev::bulk_commit();
+  }
+  fsmoe_dev::bulk_wait<0>();  // shared memory must outlive the stores
+}
+
 // ---------------------------------------------------------------- combine --
 
 template <typename T>
@@ -328,6 +379,42 @@ __device__ __forceinline__ void st8(T* row, int j, int M, const A* x) {
   }
 }
 
+// Raw 8-element vectors: loads stay packed (bf16: one uint4 = 8 values) until
+// the element is used, which keeps the in-flight loads cheap in registers
+// (fp32 staging of whole vectors cost 98 registers and 25 % occupancy).
+template <typename T>
+struct Raw8 {
+  using type = typename Acc<T>::type[8];
+};
+template <>
+struct Raw8<__nv_bfloat16> {
+  using type = uint4;
+};
+template <bool VEC, typename T>
+__device__ __forceinline__ void ldraw(const T* row, int j, int M, typename Raw8<T>::type& r) {
+  if constexpr (std::is_same_v<T, __nv_bfloat16>) {
+    if (VEC) {
+      r = *reinterpret_cast<const uint4*>(row + j);
+    } else {
+      __nv_bfloat16 h[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) h[v] = j + v < M ? row[j + v] : __float2bfloat16(0.f);
+      r = *reinterpret_cast<uint4*>(h);
+    }
+  } else {
+    ld8<VEC>(row, j, M, r);
+  }
+}
+template <typename T, typename A>
+__device__ __forceinline__ A rawget(const typename Raw8<T>::type& r, int v) {
+  if constexpr (std::is_same_v<T, __nv_bfloat16>) {
+    const uint32_t w = (&r.x)[v >> 1];
+    return __uint_as_float((v & 1) ? (w & 0xffff0000u) : (w << 16));
+  } else {
+    return r[v];
+  }
+}
+
 // y[t] = sum_{kept picks of t, pick order} w * buf[row(slot)]; one warp per token.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(256)
@@ -352,16 +439,16 @@ __global__ void __launch_bounds__(256)
       if (s < 0) continue;
       const A w = static_cast<A>(pw[p]);
       const T* br = buf + slot_row(s, E, C, chunks) * M;
-      A val[NV][CV];
+      typename Raw8<T>::type val[NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) {
         const int j = jb + (u * 32 + lane) * CV;
-        if (j < M) ld8<VEC>(br, j, M, val[u]);
+        if (j < M) ldraw<VEC>(br, j, M, val[u]);
       }
 #pragma unroll
       for (int u = 0; u < NV; ++u)
 #pragma unroll
-        for (int v = 0; v < CV; ++v) acc[u][v] = madd(acc[u][v], w, val[u][v]);
+        for (int v = 0; v < CV; ++v) acc[u][v] = madd(acc[u][v], w, rawget<T, A>(val[u], v));
     }
 #pragma unroll
     for (int u = 0; u < NV; ++u) {
@@ -400,16 +487,16 @@ __global__ void __launch_bounds__(256)
       const int s = slot_of_pick[tpick[q]];
       if (s < 0) continue;
       const T* br = dbuf + slot_row(s, E, C, chunks) * M;
-      A val[NV][CV];
+      typename Raw8<T>::type val[NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) {
         const int j = jb + (u * 32 + lane) * CV;
-        if (j < M) ld8<VEC>(br, j, M, val[u]);
+        if (j < M) ldraw<VEC>(br, j, M, val[u]);
       }
 #pragma unroll
       for (int u = 0; u < NV; ++u)
 #pragma unroll
-        for (int v = 0; v < CV; ++v) acc[u][v] = acc[u][v] + val[u][v];
+        for (int v = 0; v < CV; ++v) acc[u][v] = acc[u][v] + rawget<T, A>(val[u], v);
     }
 #pragma unroll
     for (int u = 0; u < NV; ++u) {
@@ -445,13 +532,13 @@ __global__ void __launch_bounds__(256)
   const T* o = buf + row * M;
   A dot = A(0);
   for (int jb = 0; jb < M; jb += 32 * CV * NV) {
-    A gv[NV][CV], ov[NV][CV];
+    typename Raw8<T>::type gv[NV], ov[NV];
 #pragma unroll
     for (int u = 0; u < NV; ++u) {
       const int j = jb + (u * 32 + lane) * CV;
       if (j < M) {
-        ld8<VEC>(g, j, M, gv[u]);
-        ld8<VEC>(o, j, M, ov[u]);
+        ldraw<VEC>(g, j, M, gv[u]);
+        ldraw<VEC>(o, j, M, ov[u]);
       }
     }
 #pragma unroll
@@ -461,8 +548,9 @@ __global__ void __launch_bounds__(256)
       A out[CV];
 #pragma unroll
       for (int v = 0; v < CV; ++v) {
-        out[v] = static_cast<A>(w * gv[u][v]);
-        dot = madd(dot, gv[u][v], ov[u][v]);
+        const A gvv = rawget<T, A>(gv[u], v);
+        out[v] = static_cast<A>(w * gvv);
+        dot = madd(dot, gvv, rawget<T, A>(ov[u], v));
       }
       st8<VEC>(dr, j, M, out);
     }
@@ -539,7 +627,18 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
   if (n_slots <= 0 || M <= 0) return FSMOE_OK;
   const long long row_bytes = static_cast<long long>(M) * elem_size(dtype);
   const int grid = static_cast<int>((n_slots + 7) / 8);
-  if (row_bytes % 16 == 0) {
+  if (row_bytes % 16 == 0 && row_bytes <= 4096 && !getenv("FSMOE_ROUTE_NOBULK")) {
+    const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
+      attr = true;
+    }
+    dispatch_bulk_kernel<<<static_cast<int>((n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
+        n_slots, static_cast<int>(row_bytes), E, C, chunks, pick_of_slot, ptok,
+        static_cast<const uint8_t*>(x), buf);
+    ::fsmoe::count_launch();
+  } else if (row_bytes % 16 == 0) {
     dispatch_kernel<uint4><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 16), E, C,
                                                  chunks, pick_of_slot, ptok,
                                                  static_cast<const uint4*>(x), buf); ::fsmoe::count_launch();
