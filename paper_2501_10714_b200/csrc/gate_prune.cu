@@ -531,6 +531,8 @@ __global__ void __launch_bounds__(128)
 
 constexpr int SC_TOK = 64;             // tokens per screen block
 constexpr int SC_JC = 64;              // reduction chunk (columns of x)
+constexpr int SC_STG = 4;              // cp.async pipeline depth (chunks in flight)
+constexpr int SC_MT_WARPS = 2;         // warps that run the noise draws beside the loop
 constexpr int SC_XROW = SC_JC + 8;     // bf16 per smem x row: 144 B, conflict-free LDS.128
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
@@ -560,52 +562,89 @@ __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
 
 template <int NCP, int E_MAX>
 struct ScreenSmem {
-  static constexpr int X = 2 * SC_TOK * SC_XROW * 2;       // bf16 x chunks, double-buffered
+  static constexpr int X = SC_STG * SC_TOK * SC_XROW * 2;  // bf16 x chunks
   static constexpr int XF = SC_TOK * SC_FROW * 4;          // the current chunk in fp32
-  static constexpr int W = 2 * SC_JC * NCP * 4;            // fp32 W chunks
-  static constexpr int DRAWS = SC_TOK * 2 * E_MAX * 8;     // mt19937_64 outputs
+  static constexpr int W = SC_STG * SC_JC * NCP * 4;       // fp32 W chunks
+  static constexpr int LOOP = X + XF + W;
+  // after the main loop the x / W tiles are dead and hold, in order:
+  static constexpr int PART = 3 * SC_TOK * (NCP + 1) * 4;  // split-K partials
+  static constexpr int SC = SC_TOK * (NCP + 1) * 4;        // approximate scores
   static constexpr int LOHI = SC_TOK * E_MAX * 8 * 2;      // bounds
+  static_assert(PART + SC + LOHI <= LOOP, "post-loop data fits over the tiles");
+  static constexpr int DRAWS = SC_TOK * 2 * E_MAX * 8;     // mt19937_64 outputs (own space)
   static constexpr int NRM = SC_TOK * 4 * 4;
-  static constexpr int BYTES = X + XF + W + DRAWS + LOHI + NRM;
+  static constexpr int BYTES = LOOP + DRAWS + NRM;
 };
 
 // KIND 0 noisy (NC = 2E), 1 sigmoid (NC = E); NCP = NC rounded up to 32 / 64.
 // Two thread groups split each chunk's columns of x (in-block split-K: two
 // partial FMA chains per output, summed once; covered by the bound's split
 // term). Thread (g, tx, ty): columns 4tx..4tx+3, tokens ty + 16 i (i < 4).
-constexpr int SC_GRP = 4;  // in-block split-K groups
+// in-block split-K groups: 512 GEMM threads per block (4 groups of 128 for 32
+// columns, 2 of 256 for 64 columns)
+template <int NCP>
+__host__ __device__ constexpr int sc_grp() { return 512 / (NCP * 4); }
 
+__device__ __forceinline__ void bar_sync_named(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// GEMM threads (NCP * 4 * SC_GRP) sync among themselves with named barrier 1;
+// the extra SC_MT_WARPS warps compute the noise draws meanwhile (noisy only)
+// and meet everyone at the first __syncthreads after the loop.
 template <int KIND, int NCP, int E_MAX>
-__global__ void __launch_bounds__(NCP * 4 * SC_GRP)
+__global__ void __launch_bounds__(512 + SC_MT_WARPS * 32)
     screen_kernel(const __nv_bfloat16* __restrict__ x, int T, int M, int E, int k,
                   const float* __restrict__ W32, int NC, const double* __restrict__ wn, double cB,
                   double gam, uint64_t seed, double* __restrict__ noise_ws,
                   double* __restrict__ scores_out, double* __restrict__ spread_out,
                   uint64_t* __restrict__ mask) {
   using S = ScreenSmem<NCP, E_MAX>;
+  constexpr int SC_GRP = sc_grp<NCP>();
   constexpr int NT = NCP * 4 * SC_GRP;
   constexpr int QX = NCP / 4;  // column quads
   extern __shared__ __align__(16) uint8_t sm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);
   float* xf = reinterpret_cast<float*>(sm + S::X);
   float* wsm = reinterpret_cast<float*>(sm + S::X + S::XF);
-  uint64_t* draws = reinterpret_cast<uint64_t*>(sm + S::X + S::XF + S::W);
-  double* lo = reinterpret_cast<double*>(sm + S::X + S::XF + S::W + S::DRAWS);
+  double* lo = reinterpret_cast<double*>(sm + S::PART + S::SC);
   double* hi = lo + SC_TOK * E_MAX;
-  float* nrm = reinterpret_cast<float*>(sm + S::X + S::XF + S::W + S::DRAWS + S::LOHI);
+  uint64_t* draws = reinterpret_cast<uint64_t*>(sm + S::LOOP);
+  float* nrm = reinterpret_cast<float*>(sm + S::LOOP + S::DRAWS);
   const int tid = threadIdx.x;
   const int grp = tid / (NCP * 4), lt = tid % (NCP * 4);
   const int tx = lt % QX, ty = lt / QX;
   const int t0 = blockIdx.x * SC_TOK;
   const int ntok = min(SC_TOK, T - t0);
-  // zero the padding columns of both W buffers once (cp.async only fills < NC)
-  if (NC < NCP)
-    for (int i = tid; i < 2 * SC_JC * NCP; i += NT)
+  if (tid >= NT) {
+    // ---- noise-draw warps: the seeding recurrence is sequential per token
+    const int mt_tid = tid - NT;
+    if (KIND == 0)
+      for (int tl = mt_tid; tl < ntok; tl += SC_MT_WARPS * 32) {
+        uint64_t lw[2 * E_MAX + 1];
+        uint64_t w = seed + static_cast<uint64_t>(t0 + tl);
+        lw[0] = w;
+        const int nout = 2 * E;
+        for (int i = 1; i <= nout; ++i) {
+          w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+          lw[i] = w;
+        }
+        for (int i = nout + 1; i < 156; ++i) w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+        for (int o = 0; o < nout; ++o) {
+          w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(156 + o);
+          const uint64_t y = (lw[o] & MT_UM) | (lw[o + 1] & MT_LM);
+          draws[tl * 2 * E_MAX + o] = temper(w ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL));
+        }
+      }
+  }
+  // zero the padding columns of every W buffer once (cp.async only fills < NC)
+  if (NC < NCP && tid < NT)
+    for (int i = tid; i < SC_STG * SC_JC * NCP; i += NT)
       if (i % NCP >= NC) wsm[i] = 0.f;
   const int nck = M / SC_JC;
   auto issue = [&](int ck) {
     if (ck < nck) {
-      const int b = ck & 1;
+      const int b = ck % SC_STG;
       const int j0 = ck * SC_JC;
       for (int i = tid; i < SC_TOK * (SC_JC / 8); i += NT) {
         const int r = i / (SC_JC / 8), c = i % (SC_JC / 8);
@@ -620,39 +659,22 @@ __global__ void __launch_bounds__(NCP * 4 * SC_GRP)
     }
     cp_async_commit();
   };
-  issue(0);
-  issue(1);
-  // noise draws of this block's tokens: the seeding recurrence is sequential
-  if (KIND == 0 && tid < ntok) {
-    uint64_t lw[2 * E_MAX + 1];
-    uint64_t w = seed + static_cast<uint64_t>(t0 + tid);
-    lw[0] = w;
-    const int nout = 2 * E;
-    for (int i = 1; i <= nout; ++i) {
-      w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
-      lw[i] = w;
-    }
-    for (int i = nout + 1; i < 156; ++i) w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
-    for (int o = 0; o < nout; ++o) {
-      w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(156 + o);
-      const uint64_t y = (lw[o] & MT_UM) | (lw[o + 1] & MT_LM);
-      draws[tid * 2 * E_MAX + o] = temper(w ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL));
-    }
-  }
   float2 acc[4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
   float nacc = 0.f;  // |x|^2 partial: token tid/4, quarter (tid&3) of each chunk
+  if (tid < NT) {
+  for (int s0 = 0; s0 < SC_STG - 1; ++s0) issue(s0);
   for (int ck = 0; ck < nck; ++ck) {
-    if (ck + 1 < nck) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    __syncthreads();
-    const int b = ck & 1;
+    cp_async_wait<SC_STG - 2>();  // chunk ck has landed (later ones may be in flight)
+    bar_sync_named(1, NT);
+    const int b = ck % SC_STG;
     // bf16 -> fp32 once per element (thread: token tid/4, quarter tid&3),
     // |x|^2 from the exact squares of the bf16 values
     if (tid < 4 * SC_TOK) {
       const __nv_bfloat16* xr = xs + (b * SC_TOK + (tid >> 2)) * SC_XROW + (tid & 3) * (SC_JC / 4);
       float* fr = xf + (tid >> 2) * SC_FROW + (tid & 3) * (SC_JC / 4);
+      static_assert(SC_JC % 32 == 0, "quarters of 8-element vectors");
 #pragma unroll
       for (int j = 0; j < SC_JC / 4; j += 8) {
         const uint4 u = *reinterpret_cast<const uint4*>(xr + j);
@@ -669,7 +691,7 @@ __global__ void __launch_bounds__(NCP * 4 * SC_GRP)
         *reinterpret_cast<float4*>(fr + j + 4) = make_float4(v[4], v[5], v[6], v[7]);
       }
     }
-    __syncthreads();
+    bar_sync_named(1, NT);
     const float* wb = wsm + b * SC_JC * NCP;
 #pragma unroll 2
     for (int j4 = grp * (SC_JC / 4 / SC_GRP); j4 < (grp + 1) * (SC_JC / 4 / SC_GRP); ++j4) {
@@ -688,17 +710,18 @@ __global__ void __launch_bounds__(NCP * 4 * SC_GRP)
         }
       }
     }
-    __syncthreads();
-    issue(ck + 2);
+    issue(ck + SC_STG - 1);  // into the stage chunk ck-1 used (everyone is past it)
   }
+  cp_async_wait<0>();
+  }
+  __syncthreads();
   // approximate scores -> smem: groups 1..3 park their partial sums (the
   // x tiles are free now), group 0 adds them: (g0 + g1) + (g2 + g3), two more
   // roundings per output, inside the bound's split term; |x|^2 -> nrm
   // (both over the x / fp32-x / W tiles, which are dead after the loop)
   float* part = reinterpret_cast<float*>(sm);                     // [3][SC_TOK][NCP + 1]
-  float* sc = part + 3 * SC_TOK * (NCP + 1);                      // [SC_TOK][NCP + 1]
-  static_assert(4 * SC_TOK * (NCP + 1) * 4 <= S::X + S::XF + S::W, "partials fit over the tiles");
-  if (grp > 0) {
+  float* sc = reinterpret_cast<float*>(sm + S::PART);             // [SC_TOK][NCP + 1]
+  if (grp > 0 && tid < NT) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       float* o = part + ((grp - 1) * SC_TOK + ty + 16 * i) * (NCP + 1) + 4 * tx;
@@ -718,16 +741,23 @@ __global__ void __launch_bounds__(NCP * 4 * SC_GRP)
       const float* p2 = p1 + SC_TOK * (NCP + 1);
       const float* p3 = p2 + SC_TOK * (NCP + 1);
       float* o = sc + r * (NCP + 1) + 4 * tx;
-      o[0] = (acc[i][0].x + p1[0]) + (p2[0] + p3[0]);
-      o[1] = (acc[i][0].y + p1[1]) + (p2[1] + p3[1]);
-      o[2] = (acc[i][1].x + p1[2]) + (p2[2] + p3[2]);
-      o[3] = (acc[i][1].y + p1[3]) + (p2[3] + p3[3]);
+      if constexpr (SC_GRP == 4) {
+        o[0] = (acc[i][0].x + p1[0]) + (p2[0] + p3[0]);
+        o[1] = (acc[i][0].y + p1[1]) + (p2[1] + p3[1]);
+        o[2] = (acc[i][1].x + p1[2]) + (p2[2] + p3[2]);
+        o[3] = (acc[i][1].y + p1[3]) + (p2[3] + p3[3]);
+      } else {
+        o[0] = acc[i][0].x + p1[0];
+        o[1] = acc[i][0].y + p1[1];
+        o[2] = acc[i][1].x + p1[2];
+        o[3] = acc[i][1].y + p1[3];
+      }
     }
   }
   __syncthreads();
   // bounds: |s~ - s_ref| <= cB |x|_2 |w_e|_2 (see the header); |x|^2 summed in
   // fp32 from exact bf16 squares: s <= s~ (1 + 2 gam), gam = gamma_M
-  for (int pi = tid; pi < ntok * E; pi += NT) {
+  for (int pi = tid; pi < ntok * E; pi += blockDim.x) {
     const int tl = pi / E, e = pi % E;
     const long long o = static_cast<long long>(t0 + tl) * E + e;
     const double xs2 = (static_cast<double>(nrm[4 * tl]) + static_cast<double>(nrm[4 * tl + 1])) +
@@ -983,7 +1013,7 @@ void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const floa
     attr = true;
   }
   const auto* xb = static_cast<const __nv_bfloat16*>(x);
-  screen_kernel<KIND, NCP, E_MAX><<<(T + SC_TOK - 1) / SC_TOK, NCP * 4 * SC_GRP, SMEM, st>>>(
+  screen_kernel<KIND, NCP, E_MAX><<<(T + SC_TOK - 1) / SC_TOK, 512 + SC_MT_WARPS * 32, SMEM, st>>>(
       xb, T, M, E, k, W32, NC, wn, cB, gam, d.seed, noise_ws, scores_out, spread_out, mask);
   ::fsmoe::count_launch();
   constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
