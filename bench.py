@@ -396,7 +396,9 @@ def gpu_arm(args):
                          "against compute, all inside the timed region"}
 
     timeline = None
-    if args.trace:
+    if args.trace or world > 1:
+        # measured per-phase timeline (3 extra steps, outside the timed
+        # region): with EP it carries the exposed AlltoAll
         nt = 3
         layer.set_trace(True)
         for _ in range(nt):
@@ -405,9 +407,10 @@ def gpu_arm(args):
         torch.cuda.synchronize()
         tj = layer.trace_json()
         layer.set_trace(False)
-        os.makedirs(os.path.dirname(os.path.abspath(args.trace)) or ".", exist_ok=True)
-        with open(f"{args.trace}.rank{rank}.json", "w") as f:
-            f.write(tj)
+        if args.trace:
+            os.makedirs(os.path.dirname(os.path.abspath(args.trace)) or ".", exist_ok=True)
+            with open(f"{args.trace}.rank{rank}.json", "w") as f:
+                f.write(tj)
         timeline = timeline_summary(tj, nt)
 
     roof, gflops, gms = gemm_roofline(layer, peaks)
@@ -421,7 +424,32 @@ def gpu_arm(args):
     a2a_bytes = 4 * E * C * M * 2 * (world - 1) / world
     t_gemm = gflops / (peaks.get("bf16_tflops", 1590.0) * 1e12) * 1e3
     t_a2a = a2a_bytes / (NVLINK_GBS * 1e9) * 1e3
+    a2a_meas = None
+    if world > 1:
+        # what NCCL's AlltoAll moves on this box for the step's volume (one
+        # exchange = a quarter of the step's a2a bytes), beside the 900 GB/s
+        # nominal the roofline uses
+        n = E * C * M // world * world
+        sb = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        rb = torch.empty_like(sb)
+        for _ in range(3):
+            dist.all_to_all_single(rb, sb)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(10):
+            dist.all_to_all_single(rb, sb)
+        e.record()
+        torch.cuda.synchronize()
+        ams = s.elapsed_time(e) / 10
+        tt = torch.tensor([ams], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ams = float(tt.item())
+        moved = n * 2 * (world - 1) / world
+        a2a_meas = {"nccl_alltoall_ms": ams, "bytes_out_per_gpu": moved,
+                    "busbw_gbs": moved / (ams * 1e-3) / 1e9,
+                    "note": "torch.distributed all_to_all_single (NCCL) of one dispatch's volume"}
     step_roof = {"gemm_flops": gflops, "a2a_bytes_out_per_gpu": a2a_bytes,
+                 "a2a_measured": a2a_meas,
                  "roofline_ms": max(t_gemm, t_a2a), "measured_ms": ms,
                  "frac": max(t_gemm, t_a2a) / ms, "gemm_share_of_step": gms / ms,
                  "roofline_tokens_per_s": world * T / (max(t_gemm, t_a2a) * 1e-3)}
