@@ -206,6 +206,14 @@ int fsmoe_combine_bwd_peer(int dtype, int model_dim, int experts, long long capa
                            const double* pick_weight, const void* dy, const void* buffers,
                            const fsmoe_peer_rows* d_dst, double* d_weight, void* stream);
 
+/* Row gather through the TMA engine: dst[i] = src[src_row[i]] for i < n_rows
+ * (src_row[i] < 0: a zero row); dst through dst_map when non-null (rows land
+ * in the owning rank's buffer), else the local buffer dst. With a top-1
+ * softmax gate every kept weight is exactly 1.0, so combine_tokens
+ * (workload.cpp:266-282) and its backward reduce to such gathers. */
+int fsmoe_gather_rows(int dtype, int model_dim, long long n_rows, const int* src_row,
+                      const void* src, void* dst, const fsmoe_peer_rows* dst_map, void* stream);
+
 typedef struct fsmoe_gemm_desc {
   int kind;        /* 0 row-grouped (fwd/dgrad), 1 k-grouped (wgrad) */
   int nblk, rows, K, N, Mo, No, n_w;

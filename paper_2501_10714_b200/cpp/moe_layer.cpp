@@ -172,6 +172,10 @@ struct MoELayer::Impl {
   // the grouped ncclSend/ncclRecv baseline). The four receive-side buffers,
   // the received fills and the arrival flags live in one IPC-shared region;
   // producers store rows straight into the owner's copy.
+  // top-1 softmax gate (noisy / cosine): the masked softmax over one survivor
+  // is exactly 1.0 (workload.cpp:123-133), so the I-order and its backward
+  // are row gathers and the weight gradient is identically zero
+  bool unit_top1 = false;
   bool peer = false;
   void* sym = nullptr;
   std::vector<void*> sym_peers;
@@ -519,6 +523,11 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   throw_on(fsmoe_gate_validate(&d));
   I.n_picks = cfg.gate == GateKind::expert_choice ? static_cast<long long>(I.E) * d.top_k
                                                   : static_cast<long long>(I.T) * I.k;
+  I.unit_top1 = cfg.top_k == 1 &&
+                (cfg.gate == GateKind::noisy_topk || cfg.gate == GateKind::cosine_topk) &&
+                static_cast<long long>(I.M) * (cfg.precision == Precision::bf16 ? 2 : 4) % 16 == 0 &&
+                static_cast<long long>(I.M) * (cfg.precision == Precision::bf16 ? 2 : 4) <= 4096 &&
+                !std::getenv("FSMOE_NO_UNIT_TOP1");
   if (cfg.gate == GateKind::expert_choice && I.C > I.T)
     throw ConfigError("gate: expert capacity exceeds token count");
 
@@ -685,8 +694,11 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
   }
   // K5 combine
   sp = I.tr.begin("i-order", 2, I.s_comp);
-  throw_on(fsmoe_combine(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.w, I.Os, y,
-                         I.s_comp));
+  if (I.unit_top1)  // every kept weight is exactly 1.0: y[t] = O[slot(t)] (0 if dropped)
+    throw_on(fsmoe_gather_rows(I.dtype, I.M, I.T, I.slot, I.Os, y, nullptr, I.s_comp));
+  else
+    throw_on(fsmoe_combine(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.w, I.Os, y,
+                           I.s_comp));
   I.tr.end(sp, I.s_comp);
   I.last_was_bwd = false;
   I.record(I.ev_out, I.s_comp);
@@ -719,8 +731,11 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
     }
     // I-order backward fused with the dispatch AlltoAll of dO
     sp = I.tr.begin("i-order", 2, I.s_comp);
-    throw_on(fsmoe_combine_bwd_peer(I.dtype, I.M, I.E, I.C, I.n_picks, I.pos, I.tok, I.w, dy, I.Os,
-                                    &I.map_dO, I.dw, I.s_comp));
+    if (I.unit_top1)  // dO[slot] = 1.0 * dy[token]; d_weight feeds no gradient (gate_bwd.cu)
+      throw_on(fsmoe_dispatch_peer(I.dtype, I.M, I.E, I.C, I.pos, I.tok, dy, &I.map_dO, I.s_comp));
+    else
+      throw_on(fsmoe_combine_bwd_peer(I.dtype, I.M, I.E, I.C, I.n_picks, I.pos, I.tok, I.w, dy, I.Os,
+                                      &I.map_dO, I.dw, I.s_comp));
     I.tr.end(sp, I.s_comp);
     sp = I.tr.begin("dispatch", 0, I.s_comp);
     I.peer_signal(I.slot_disp_bwd());
@@ -749,8 +764,11 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
   } else {
   // I-order backward: dO (send side) and d weights
   sp = I.tr.begin("i-order", 2, I.s_comp);
-  throw_on(fsmoe_combine_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.n_picks, I.pos, I.tok, I.w, I.slot,
-                             dy, I.Os, I.dOs, I.dw, I.s_comp));
+  if (I.unit_top1)
+    throw_on(fsmoe_dispatch(I.dtype, I.M, I.E, I.C, 1, I.pos, I.tok, dy, I.dOs, I.s_comp));
+  else
+    throw_on(fsmoe_combine_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.n_picks, I.pos, I.tok, I.w, I.slot,
+                               dy, I.Os, I.dOs, I.dw, I.s_comp));
   I.tr.end(sp, I.s_comp);
   if (I.P > 1) {
     I.record(I.ev_gate, I.s_comp);
@@ -786,8 +804,11 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
   }
   // Order backward, then the gate's contribution to dx and its parameters
   sp = I.tr.begin("order", 2, I.s_comp);
-  throw_on(fsmoe_dispatch_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.dXs, dx,
-                              0, I.s_comp));
+  if (I.unit_top1)  // dx[t] = dX[slot(t)] (0 if dropped)
+    throw_on(fsmoe_gather_rows(I.dtype, I.M, I.T, I.slot, I.dXs, dx, nullptr, I.s_comp));
+  else
+    throw_on(fsmoe_dispatch_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.dXs, dx,
+                                0, I.s_comp));
   I.tr.end(sp, I.s_comp);
   if (!I.x_last) throw ConfigError("layer: backward before forward");
   sp = I.tr.begin("gate", 2, I.s_comp);

@@ -229,3 +229,17 @@ int fsmoe_gate_bwd(const fsmoe_gate_desc* d, const void* x, const double* w_scor
 }
 
 }  // extern "C"
+
+int fsmoe_gather_rows(int dtype, int model_dim, long long n_rows, const int* src_row,
+                      const void* src, void* dst, const fsmoe_peer_rows* dst_map, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (model_dim <= 0) return config_error("gather_rows: model_dim must be positive");
+  const long long rb = static_cast<long long>(model_dim) * (dtype == FSMOE_F64 ? 8 : dtype == FSMOE_F32 ? 4 : 2);
+  if (dst_map) {
+    if (dst_map->world < 1 || dst_map->world > FSMOE_MAX_PEERS || dst_map->experts_local < 1 ||
+        dst_map->capacity < 1)
+      return config_error("gather_rows: bad peer map");
+    return gather_rows_launch(n_rows, rb, src_row, src, peer_rows_of(dst_map), as_stream(stream));
+  }
+  return gather_rows_launch(n_rows, rb, src_row, src, local_rows(dst), as_stream(stream));
+}

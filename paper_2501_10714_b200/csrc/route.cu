@@ -271,6 +271,42 @@ __global__ void __launch_bounds__(32)
   fsmoe_dev::bulk_wait<0>();  // shared memory must outlive the stores
 }
 
+// dst[i] = src[idx[i]] (idx < 0: zero row), i < n_rows, through the TMA
+// engine like dispatch_bulk_kernel; dst through a peer map (identity for a
+// local buffer). The I-order / order-backward permutations of a top-1
+// softmax gate (every kept weight is exactly 1.0) are such gathers.
+__global__ void __launch_bounds__(32)
+    gather_bulk_kernel(long long n_rows, int row_bytes, const int* __restrict__ idx,
+                       const uint8_t* __restrict__ src, const PeerRows dst) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int lane = threadIdx.x;
+  const long long i = blockIdx.x * static_cast<long long>(BK_ROWS) + lane;
+  uint8_t* zero = sm + BK_ROWS * row_bytes;
+  for (int b = lane * 16; b < row_bytes; b += 32 * 16) *reinterpret_cast<uint4*>(zero + b) = make_uint4(0, 0, 0, 0);
+  if (lane == 0) {
+    fsmoe_dev::mbar_init(&bar, 32);
+    fsmoe_dev::fence_barrier_init();
+  }
+  __syncwarp();
+  const bool valid = i < n_rows;
+  const int s = valid ? idx[i] : -1;
+  uint8_t* mine = sm + lane * row_bytes;
+  if (s >= 0) {
+    fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
+    fsmoe_dev::bulk_load(mine, src + static_cast<long long>(s) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
+  } else {
+    fsmoe_dev::mbar_arrive(&bar);
+  }
+  fsmoe_dev::fence_proxy_async_smem();
+  fsmoe_dev::mbar_wait(&bar, 0);
+  if (valid) {
+    bulk_store(peer_row(dst, i, row_bytes), s >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
+    fsmoe_dev::bulk_commit();
+  }
+  fsmoe_dev::bulk_wait<0>();
+}
+
 // ---------------------------------------------------------------- combine --
 
 template <typename T>
@@ -619,6 +655,23 @@ int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, in
   if (pb > 0) { tok_place_kernel<<<pb, 256, 0, st>>>(P, ptok, T, tptr, cursor, tpick); ::fsmoe::count_launch(); }
   tok_sort_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, tptr, tpick); ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_token_index");
+}
+
+int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, const void* src,
+                       const PeerRows& dst, cudaStream_t st) {
+  if (n_rows <= 0) return FSMOE_OK;
+  if (row_bytes % 16 != 0 || row_bytes > 4096)
+    return config_error("gather_rows: row bytes must be a multiple of 16 and at most 4096");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
+    attr = true;
+  }
+  gather_bulk_kernel<<<static_cast<int>((n_rows + BK_ROWS - 1) / BK_ROWS), 32,
+                       static_cast<int>((BK_ROWS + 1) * row_bytes), st>>>(
+      n_rows, static_cast<int>(row_bytes), idx, static_cast<const uint8_t*>(src), dst);
+  ::fsmoe::count_launch();
+  return cuda_status(cudaGetLastError(), "fsmoe_gather_rows");
 }
 
 int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int* pick_of_slot,

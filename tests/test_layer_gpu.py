@@ -126,3 +126,18 @@ def test_trace_timeline_has_every_phase_and_same_results():
         assert n in names, (n, names)
     assert all(e["dur"] >= 0 and e["ts"] >= 0 for e in tr["traceEvents"])
     layer.close()
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+@pytest.mark.parametrize("gate", ["noisy_topk", "cosine_topk"])
+def test_top1_softmax_gathers_match_weighted_path(precision, gate, monkeypatch):
+    """Top-1 softmax gates: every kept weight is exactly 1.0, so the layer runs
+    the I-order and its backward as row gathers (fsmoe_gather_rows /
+    dispatch of dy). Same results as the weighted kernels, bit for bit, and
+    the restatement within tolerance (capacity 48 < T*k/E: real drops)."""
+    layer, y, dx, yr, ref = _run(gate, "simple", precision, k=1, cap=48)
+    assert _rel(y, yr) < TOL[precision]
+    assert _rel(dx, ref["dx"]) < TOL[precision]
+    monkeypatch.setenv("FSMOE_NO_UNIT_TOP1", "1")
+    _, y2, dx2, _, _ = _run(gate, "simple", precision, k=1, cap=48)
+    assert torch.equal(y, y2) and torch.equal(dx, dx2)
