@@ -630,9 +630,12 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
   if (I.peer) I.peer_signal(I.slot_bar_fwd());
   // K1 gate, K2 assign, token index, K3 dispatch
   int sp = I.tr.begin("gate", 2, I.s_comp);
+  // a top-1 softmax gate has no gradient: its saved tensors are not needed
+  // (and the gate may then skip the exact logits of tokens with one candidate)
+  const bool save = !I.unit_top1;
   throw_on(fsmoe_gate(&I.gd, x, I.prm.w_gate, I.prm.w_noise, I.prm.proj, I.tok, I.exp, I.w,
-                      I.scores, I.noise, I.spread, I.proj_out, I.status, I.gate_ws, I.gate_wsb,
-                      I.s_comp));
+                      save ? I.scores : nullptr, save ? I.noise : nullptr, save ? I.spread : nullptr,
+                      I.proj_out, I.status, I.gate_ws, I.gate_wsb, I.s_comp));
   I.tr.end(sp, I.s_comp);
   sp = I.tr.begin("order", 2, I.s_comp);
   throw_on(fsmoe_assign(I.n_picks, I.tok, I.exp, I.T, I.E, I.C, I.slot, I.fill, I.dropped, I.pos,

@@ -864,12 +864,14 @@ __global__ void __launch_bounds__(XF_THREADS)
     }
     cp_async_commit();
   };
-  issue(0);
-  issue(1);
+  // Top-1 softmax with no saved scores requested: a token whose bound leaves a
+  // single candidate has a certain pick and weight exactly 1.0 (softmax over
+  // one survivor, workload.cpp:123-133) -- its exact logits are never needed
+  const bool certain_ok = KIND == 0 && k == 1 && !scores_out && !spread_out;
   if (tid < XF_TOK) {
     const uint64_t m = tid < ntok ? mask[t0 + tid] : 0ULL;
     msk[tid] = m;
-    cnt[tid] = __popcll(m);
+    cnt[tid] = (certain_ok && __popcll(m) == 1) ? 0 : __popcll(m);
   }
   __syncthreads();
   if (tid < 32) {  // exclusive scan of the 64 counts by one warp
@@ -882,10 +884,12 @@ __global__ void __launch_bounds__(XF_THREADS)
     }
     const int tot0 = __shfl_sync(0xffffffffu, a0, 31);
     int w0 = a0 - c0, w1 = tot0 + a1 - c1;
-    for (uint64_t mm = msk[tid]; mm; mm &= mm - 1)
-      items[w0++] = make_short2(static_cast<short>(tid), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
-    for (uint64_t mm = msk[tid + 32]; mm; mm &= mm - 1)
-      items[w1++] = make_short2(static_cast<short>(tid + 32), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
+    if (c0)
+      for (uint64_t mm = msk[tid]; mm; mm &= mm - 1)
+        items[w0++] = make_short2(static_cast<short>(tid), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
+    if (c1)
+      for (uint64_t mm = msk[tid + 32]; mm; mm &= mm - 1)
+        items[w1++] = make_short2(static_cast<short>(tid + 32), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
     if (tid == 31) nitems = tot0 + a1;
   }
   __syncthreads();
@@ -900,7 +904,12 @@ __global__ void __launch_bounds__(XF_THREADS)
   int pj0 = 0, pj1 = 0;
   if (it0 < nwork) { te0 = items[it0 % nc]; pj0 = it0 / nc; }
   if (it1 < nwork) { te1 = items[it1 % nc]; pj1 = it1 / nc; }
-  const int nck = (M + XF_JC - 1) / XF_JC;
+  // stream the token / weight rows only when this block has dot products
+  const int nck = nwork > 0 ? (M + XF_JC - 1) / XF_JC : 0;
+  if (nck > 0) {
+    issue(0);
+    issue(1);
+  }
   for (int ck = 0; ck < nck; ++ck) {
     if (ck + 1 < nck) cp_async_wait<1>();
     else cp_async_wait<0>();
@@ -945,6 +954,12 @@ __global__ void __launch_bounds__(XF_THREADS)
   const int t = t0 + tid;
   const uint64_t cand = msk[tid];
   const long long row = static_cast<long long>(t) * E;
+  if (certain_ok && __popcll(cand) == 1) {
+    pick_token[t] = t;
+    pick_expert[t] = __ffsll(static_cast<long long>(cand)) - 1;
+    pick_weight[t] = 1.0;
+    return;
+  }
   double* s = ex[0][tid];
   for (uint64_t m = cand; m; m &= m - 1) {
     const int e = __ffsll(static_cast<long long>(m)) - 1;
