@@ -874,6 +874,101 @@ __global__ void __launch_bounds__(XF_THREADS)
     cnt[tid] = (certain_ok && __popcll(m) == 1) ? 0 : __popcll(m);
   }
   __syncthreads();
+  if (certain_ok) {
+    // Tokens whose fp32 bound left 2+ candidates: decide with fp64 dot
+    // products summed warp-parallel (FMA, 32 partial chains of M/32 terms + 5
+    // shuffle levels) and a rigorous bound on their distance from the
+    // reference's sequential sums -- |seq - par| <= (gamma_M + gamma_{M/32+5})
+    // sum|x_j w_j| -- plus the noise / softplus / final-add roundings. A
+    // decided token gets its certain pick (weight 1.0); an undecided one
+    // (ties, near ties) keeps its candidates for the sequential reference
+    // chain below. One warp per (token, candidate, projection) dot product.
+    __shared__ int nref;
+    __shared__ unsigned char ref_tok[XF_TOK];
+    double* rd = reinterpret_cast<double*>(sm);              // [XF_TOK][E_MAX][2] dots
+    double* ra = rd + XF_TOK * E_MAX * 2;                    // same, sum |x w|
+    if (tid == 0) {
+      int n = 0;
+      for (int tl = 0; tl < ntok; ++tl)
+        if (__popcll(msk[tl]) >= 2) ref_tok[n++] = static_cast<unsigned char>(tl);
+      nref = n;
+    }
+    __syncthreads();
+    if (nref > 0) {
+      const int warp = tid >> 5, lane = tid & 31;
+      const int nit = nref * E_MAX * 2;
+      for (int it = warp; it < nit; it += XF_THREADS / 32) {
+        const int r = it / (E_MAX * 2), e = (it / 2) % E_MAX, pj = it & 1;
+        const int tl = ref_tok[r];
+        if (e >= E || !((msk[tl] >> e) & 1ULL)) continue;
+        const __nv_bfloat16* xr = x + static_cast<long long>(t0 + tl) * M;
+        const double* wr = WT + static_cast<long long>(pj * E + e) * M;
+        double d = 0.0, aa = 0.0;
+#pragma unroll 4
+        for (int j0 = lane * 8; j0 < M; j0 += 256) {
+          const uint4 uu = __ldg(reinterpret_cast<const uint4*>(xr + j0));
+          const uint32_t w4[4] = {uu.x, uu.y, uu.z, uu.w};
+          double2 wv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) wv[q] = __ldg(reinterpret_cast<const double2*>(wr + j0 + 2 * q));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double x0 = static_cast<double>(__uint_as_float(w4[q] << 16));
+            const double x1 = static_cast<double>(__uint_as_float(w4[q] & 0xffff0000u));
+            d = __fma_rn(x0, wv[q].x, d);
+            d = __fma_rn(x1, wv[q].y, d);
+            aa = __fma_rn(fabs(x0), fabs(wv[q].x), aa);
+            aa = __fma_rn(fabs(x1), fabs(wv[q].y), aa);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          d += __shfl_xor_sync(0xffffffffu, d, o);
+          aa += __shfl_xor_sync(0xffffffffu, aa, o);
+        }
+        if (lane == 0) {
+          rd[(r * E_MAX + e) * 2 + pj] = d;
+          ra[(r * E_MAX + e) * 2 + pj] = aa * (1.0 + 1e-12);
+        }
+      }
+      __syncthreads();
+      if (tid < nref) {
+        const int tl = ref_tok[tid];
+        const uint64_t m = msk[tl];
+        const double u = 0x1.0p-53;
+        const double np = M / 32.0 + 5.0;  // terms per lane chain + shuffle levels
+        const double g = (M * u / (1.0 - M * u) + np * u / (1.0 - np * u)) * 1.01;
+        double best_s = 0.0, best_b = 0.0, other_hi = -1.0 / 0.0;
+        int best = -1;
+        for (uint64_t mm = m; mm; mm &= mm - 1) {
+          const int e = __ffsll(static_cast<long long>(mm)) - 1;
+          const double d0 = rd[(tid * E_MAX + e) * 2], d1 = rd[(tid * E_MAX + e) * 2 + 1];
+          const double a0 = ra[(tid * E_MAX + e) * 2], a1 = ra[(tid * E_MAX + e) * 2 + 1];
+          const double n = noise[static_cast<long long>(t0 + tl) * E + e];
+          const double soft = log1p(exp(d1));
+          const double sv = d0 + n * soft;
+          const double b = g * (a0 + fabs(n) * a1) +
+                           8.0 * u * (fabs(d0) + fabs(n * soft) + fabs(n) * soft) + 1e-300;
+          // best by value (ascending index: a later candidate must be larger);
+          // every other candidate's upper bound is tracked in other_hi
+          if (best < 0 || sv > best_s) {
+            if (best >= 0) other_hi = fmax(other_hi, best_s + best_b);
+            best = e;
+            best_s = sv;
+            best_b = b;
+          } else {
+            other_hi = fmax(other_hi, sv + b);
+          }
+        }
+        // certain iff the winner's lower bound clears every other upper bound
+        if (best_s - best_b > other_hi) {
+          msk[tl] = 1ULL << best;
+          cnt[tl] = 0;
+        }
+      }
+      __syncthreads();
+    }
+  }
   if (tid < 32) {  // exclusive scan of the 64 counts by one warp
     const int c0 = cnt[tid], c1 = cnt[tid + 32];
     int a0 = c0, a1 = c1;
@@ -904,8 +999,49 @@ __global__ void __launch_bounds__(XF_THREADS)
   int pj0 = 0, pj1 = 0;
   if (it0 < nwork) { te0 = items[it0 % nc]; pj0 = it0 / nc; }
   if (it1 < nwork) { te1 = items[it1 % nc]; pj1 = it1 / nc; }
-  // stream the token / weight rows only when this block has dot products
-  const int nck = nwork > 0 ? (M + XF_JC - 1) / XF_JC : 0;
+  // A block with only a handful of dot products (the few tokens whose bound
+  // leaves 2+ candidates) bulk-loads just those rows and runs each chain from
+  // shared memory with no per-chunk barriers: the chain's latency, not the
+  // staging pipeline, is then the block's time.
+  __shared__ __align__(8) uint64_t sbar;
+  const long long small_bytes = static_cast<long long>(nwork) * M * 10;
+  const bool small = nwork > 0 && small_bytes <= S::BYTES && M % 8 == 0;
+  if (small) {
+    if (tid == 0) {
+      fsmoe_dev::mbar_init(&sbar, 1);
+      fsmoe_dev::fence_barrier_init();
+      fsmoe_dev::mbar_arrive_expect_tx(&sbar, static_cast<uint32_t>(small_bytes));
+      for (int it = 0; it < nwork; ++it) {
+        const short2 te = items[it % nc];
+        const int pj = it / nc;
+        uint8_t* d = sm + static_cast<long long>(it) * M * 10;
+        fsmoe_dev::bulk_load(d, x + static_cast<long long>(t0 + te.x) * M, static_cast<uint32_t>(M * 2), &sbar);
+        fsmoe_dev::bulk_load(d + M * 2, WT + static_cast<long long>(pj * E + te.y) * M,
+                             static_cast<uint32_t>(M * 8), &sbar);
+      }
+    }
+    __syncthreads();
+    if (tid < nwork) {
+      fsmoe_dev::mbar_wait(&sbar, 0);
+      const uint8_t* xr = sm + static_cast<long long>(tid) * M * 10;
+      const double* wr = reinterpret_cast<const double*>(xr + M * 2);
+      double acc = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < M; j += 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(xr + 2 * j);
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 wv = *reinterpret_cast<const double2*>(wr + j + 2 * q);
+          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] << 16)), wv.x));
+          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] & 0xffff0000u)), wv.y));
+        }
+      }
+      ex[pj0][te0.x][te0.y] = acc;
+    }
+  }
+  // otherwise stream the token / weight rows in chunks (when there is work)
+  const int nck = (nwork > 0 && !small) ? (M + XF_JC - 1) / XF_JC : 0;
   if (nck > 0) {
     issue(0);
     issue(1);
@@ -936,8 +1072,8 @@ __global__ void __launch_bounds__(XF_THREADS)
     __syncthreads();
     issue(ck + 2);
   }
-  if (it0 < nwork) ex[pj0][te0.x][te0.y] = acc0;
-  if (it1 < nwork) ex[pj1][te1.x][te1.y] = acc1;
+  if (!small && it0 < nwork) ex[pj0][te0.x][te0.y] = acc0;
+  if (!small && it1 < nwork) ex[pj1][te1.x][te1.y] = acc1;
   // more than 2 * XF_THREADS dot products: the rest from global memory
   for (int it = it1 + XF_THREADS; it < nwork; it += XF_THREADS) {
     const short2 te = items[it % nc];

@@ -15,8 +15,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 # launches per step: skip the 3 warm-up steps of GEMMs (6 each)
 ncu --set full --clock-control none --import-source on -k regex:grouped_gemm_kernel -s 18 -c 6 \
     -o $OUT/gemm_full -f $CMD > $OUT/ncu_gemm.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:approx_scores -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:screen_kernel -s 3 -c 1 \
     -o $OUT/gate_full -f $CMD > $OUT/ncu_gate.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:dispatch_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:dispatch_bulk_kernel -s 3 -c 1 \
     -o $OUT/dispatch_full -f $CMD > $OUT/ncu_dispatch.log 2>&1
 ls -la $OUT
