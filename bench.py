@@ -34,10 +34,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MoE layer fwd+bwd tokens/sec at 1/2/4/8 B200; % of GEMM/NVLink roofline"
-WORKLOAD = dict(workload="gpt2-medium-shape MoE layer (BASELINE configs[1])", tokens_per_gpu=16384,
-                d_model=1024, d_ffn=4096, experts=16, top_k=1, gate="noisy_topk (Switch top-1)",
-                ffn="simple (GELU)", capacity_factor=1.0, dtype="bf16 / fp32 accumulate",
-                l2="inputs and activations larger than L2 (126 MB): no flush needed")
+WORKLOADS = {
+    # the headline (configs[1]): fits one GPU, EP over 2/4/8 with fixed tokens per GPU
+    "gpt2m": dict(workload="gpt2-medium-shape MoE layer (BASELINE configs[1])", tokens_per_gpu=16384,
+                  d_model=1024, d_ffn=4096, experts=16, top_k=1, gate="noisy_topk (Switch top-1)",
+                  ffn="simple (GELU)", capacity_factor=1.0, dtype="bf16 / fp32 accumulate",
+                  l2="inputs and activations larger than L2 (126 MB): no flush needed"),
+    # configs[2]: Mixtral-8x7B-shape layer, 32k tokens per GPU, 8 experts top-2
+    # SwiGLU; on N GPUs each rank holds 8/N experts (N = 8: one expert per GPU;
+    # N = 1 runs the same per-GPU expert GEMM work with all 8 experts local)
+    "mixtral": dict(workload="Mixtral-8x7B-shape MoE layer (BASELINE configs[2])", tokens_per_gpu=32768,
+                    d_model=4096, d_ffn=14336, experts=8, top_k=2, gate="noisy_topk (GShard top-2)",
+                    ffn="gated3 (SwiGLU)", capacity_factor=1.0, dtype="bf16 / fp32 accumulate",
+                    l2="inputs and activations larger than L2 (126 MB): no flush needed"),
+}
+WORKLOAD = WORKLOADS["gpt2m"]
 NVLINK_GBS = 900.0  # nominal per direction per GPU (measured peer copy ~770)
 
 
@@ -128,7 +139,7 @@ def cpu_reference_rate(seconds: float, threads: int, tokens_per_call: int, x, w_
         o = orcs[i]
         while not stop[0]:
             xs = x[(i * tokens_per_call) % x.shape[0]:][:tokens_per_call]
-            g = o.run_gate("noisy_topk", 1, 7, xs, w_gate, w_noise)
+            g = o.run_gate("noisy_topk", WORKLOAD["top_k"], 7, xs, w_gate, w_noise)
             d = o.dispatch(xs, experts, g.token, g.expert, capacity_per_call)
             o.combine(d.buffers, xs.shape[0], experts, g.token, g.expert, g.weight, d.slot_of_pick,
                       xs.shape[1])
@@ -163,7 +174,7 @@ def reference_arm(args):
     M, E, T = WORKLOAD["d_model"], WORKLOAD["experts"], 1024
     threads = os.cpu_count() or 1
     x, wg, wn = cpu_inputs(T * threads, M, E)
-    cap = -(-T // E)  # capacity_tokens(k=1, f=1.0) for the sample's B*L
+    cap = -(-T * WORKLOAD["top_k"] // E)  # capacity_tokens(k, f=1.0) for the sample's B*L
     for _ in range(args.warmup):
         cpu_reference_rate(0.2, threads, T, x, wg, wn, E, cap)
     rates, walls, kind = [], [], "port"
@@ -181,7 +192,7 @@ def reference_arm(args):
                        "(the reference has no expert FFN and no backward)"),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
                          "sample": f"{threads} threads x {T} tokens per call, d_model {M}, "
-                                   f"{E} experts, top-1, ~1 s per step"},
+                                   f"{E} experts, top-{WORKLOAD['top_k']}, ~1 s per step"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -293,9 +304,9 @@ def gpu_arm(args):
     peaks, peak_kind = load_peaks()
     T, M, H, E = (WORKLOAD["tokens_per_gpu"], WORKLOAD["d_model"], WORKLOAD["d_ffn"],
                   WORKLOAD["experts"])
-    cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=1, gate="noisy_topk",
-                    ffn="simple", capacity_factor=1.0, precision="bf16", seed=7,
-                    r_fwd=args.r_fwd, r_bwd=args.r_bwd)
+    cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=WORKLOAD["top_k"],
+                    gate="noisy_topk", ffn=WORKLOAD["ffn"].split()[0], capacity_factor=1.0,
+                    precision="bf16", seed=7, r_fwd=args.r_fwd, r_bwd=args.r_bwd)
     ep = EpGroup(world, rank, local, max_ctas=args.nccl_ctas) if world > 1 else None
     layer = MoELayer(cfg, ep, init_seed=1)
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
@@ -459,9 +470,9 @@ def gpu_arm(args):
         xs, wg, wn = cpu_inputs(1024 * (os.cpu_count() or 1), M, E)
         thr = os.cpu_count() or 1
         rate, kind, thr, calls, wall = cpu_reference_rate(args.cpu_seconds, thr, 1024, xs, wg, wn, E,
-                                                          -(-1024 // E))
+                                                          -(-1024 * WORKLOAD["top_k"] // E))
         cpu = {"value": rate, "unit": "tokens/s", "cores": thr, "kind": kind,
-               "sample": f"{calls} calls x 1024 tokens (d_model {M}, {E} experts, top-1) of "
+               "sample": f"{calls} calls x 1024 tokens (d_model {M}, {E} experts, top-{WORKLOAD['top_k']}) of "
                          f"run_gate->dispatch_tokens->combine_tokens over {wall:.1f} s on {thr} "
                          "threads; the reference has no FFN/backward"}
 
@@ -499,8 +510,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", default="", help="write per-rank measured timelines to PATH.rankN.json")
+    ap.add_argument("--config", default="gpt2m", choices=sorted(WORKLOADS),
+                    help="gpt2m = BASELINE configs[1] (the headline); mixtral = configs[2]")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    global WORKLOAD
+    WORKLOAD = WORKLOADS[args.config]
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return

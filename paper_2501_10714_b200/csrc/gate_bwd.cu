@@ -130,37 +130,42 @@ constexpr int XT_TCH = 256;  // tokens per partial
 constexpr int XT_J = 64;
 constexpr int XT_C = 16;
 
-// partial[chunk][j][c] = sum_{t in chunk} X(t, j) * G(t, c)
-template <int DT>
+// partial[chunk][j][c] = sum_{t in chunk} X(t, j) * G(t, c).
+// A = the arithmetic type: fp64 for fp64 tokens; fp32 for bf16 / fp32 tokens
+// (exact in fp32) -- the gate gradient has no reference counterpart (the
+// reference has no backward), B200's fp64 pipe is a small fraction of its
+// fp32 rate, and 256-token fp32 partials summed in fp64 keep the relative
+// error near 1e-6, far inside the layer's gradient tolerances.
+template <int DT, typename A>
 __global__ void __launch_bounds__(XT_J * XT_C)
     xtg_partial_kernel(int T, int M, int NC, const void* __restrict__ X,
                        const double* __restrict__ G, long long gst, long long gsc,
                        double* __restrict__ part) {
-  __shared__ double xs[32][XT_J];
-  __shared__ double gs[32][XT_C];
+  __shared__ A xs[32][XT_J];
+  __shared__ A gs[32][XT_C];
   const int chunk = blockIdx.z;
   const int j0 = blockIdx.x * XT_J, c0 = blockIdx.y * XT_C;
   const int jj = threadIdx.x % XT_J, cc = threadIdx.x / XT_J;
-  double acc = 0.0;
+  A acc = A(0);
   const int t_end = min(T, (chunk + 1) * XT_TCH);
   for (int t0 = chunk * XT_TCH; t0 < t_end; t0 += 32) {
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * XT_J; i += XT_J * XT_C) {
       int tt = i / XT_J, j = i % XT_J;
       int t = t0 + tt;
-      xs[tt][j] = (t < t_end && j0 + j < M) ? load_as_double<DT>(X, static_cast<long long>(t) * M + j0 + j) : 0.0;
+      xs[tt][j] = (t < t_end && j0 + j < M) ? static_cast<A>(load_as_double<DT>(X, static_cast<long long>(t) * M + j0 + j)) : A(0);
     }
     for (int i = threadIdx.x; i < 32 * XT_C; i += XT_J * XT_C) {
       int tt = i / XT_C, c = i % XT_C;
       int t = t0 + tt;
-      gs[tt][c] = (t < t_end && c0 + c < NC) ? G[t * gst + (c0 + c) * gsc] : 0.0;
+      gs[tt][c] = (t < t_end && c0 + c < NC) ? static_cast<A>(G[t * gst + (c0 + c) * gsc]) : A(0);
     }
     __syncthreads();
 #pragma unroll 8
     for (int tt = 0; tt < 32; ++tt) acc += xs[tt][jj] * gs[tt][cc];
   }
   if (j0 + jj < M && c0 + cc < NC)
-    part[(static_cast<long long>(chunk) * M + j0 + jj) * NC + c0 + cc] = acc;
+    part[(static_cast<long long>(chunk) * M + j0 + jj) * NC + c0 + cc] = static_cast<double>(acc);
 }
 
 // out[j*osj + c*osc] (+)= sum_chunk partial[chunk][j][c]  (fixed order)
@@ -176,35 +181,111 @@ __global__ void xtg_reduce_kernel(int nchunks, int M, int NC, const double* __re
   *o = accumulate ? *o + a : a;
 }
 
-// dx[t][j] += sum_c G(t,c) * W(j,c)
-template <typename T>
+// dx[t][j] += sum_c G(t,c) * W(j,c)   (arithmetic type A as above)
+template <typename T, typename A>
 __global__ void __launch_bounds__(256)
     dx_acc_kernel(int Tn, int M, int NC, const double* __restrict__ G, long long gst,
                   long long gsc, const double* __restrict__ W, long long wsj, long long wsc,
                   T* __restrict__ dx) {
   const int j = blockIdx.x * 256 + threadIdx.x;
   const int t0 = blockIdx.y * 32;
-  __shared__ double gs[32][64];
+  __shared__ A gs[32][64];
   for (int c0 = 0; c0 < NC; c0 += 64) {
     const int nc = min(64, NC - c0);
-    double wr[64];
+    A wr[64];
     if (j < M)
-      for (int c = 0; c < nc; ++c) wr[c] = W[j * wsj + (c0 + c) * wsc];
+      for (int c = 0; c < nc; ++c) wr[c] = static_cast<A>(W[j * wsj + (c0 + c) * wsc]);
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * 64; i += 256) {
       int tt = i / 64, c = i % 64;
-      gs[tt][c] = (t0 + tt < Tn && c < nc) ? G[(t0 + tt) * gst + (c0 + c) * gsc] : 0.0;
+      gs[tt][c] = (t0 + tt < Tn && c < nc) ? static_cast<A>(G[(t0 + tt) * gst + (c0 + c) * gsc]) : A(0);
     }
     __syncthreads();
     if (j < M) {
       for (int tt = 0; tt < 32 && t0 + tt < Tn; ++tt) {
-        double a = 0.0;
+        A a = A(0);
         for (int c = 0; c < nc; ++c) a += gs[tt][c] * wr[c];
         T* p = dx + static_cast<long long>(t0 + tt) * M + j;
         if constexpr (sizeof(T) == 2) *p = __float2bfloat16(__bfloat162float(*p) + static_cast<float>(a));
-        else *p = static_cast<T>(static_cast<double>(*p) + a);
+        else *p = static_cast<T>(static_cast<double>(*p) + static_cast<double>(a));
       }
     }
+  }
+}
+
+// Register-tiled replacements (the gate gradient contractions are skinny:
+// NC = E or P columns): thread = one model column j, all NC accumulators in
+// registers (NCT = NC rounded up), the chunk's G rows broadcast from shared
+// memory, x read coalesced along j. Same fixed per-chunk order, so results
+// stay deterministic.
+template <int DT, typename A, int NCT>
+__global__ void __launch_bounds__(256)
+    xtg2_kernel(int T, int M, int NC, const void* __restrict__ X, const double* __restrict__ G,
+                long long gst, long long gsc, double* __restrict__ part) {
+  __shared__ A gs[32][NCT];
+  const int chunk = blockIdx.y;
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  A acc[NCT];
+#pragma unroll
+  for (int c = 0; c < NCT; ++c) acc[c] = A(0);
+  const int t_end = min(T, (chunk + 1) * XT_TCH);
+  for (int t0 = chunk * XT_TCH; t0 < t_end; t0 += 32) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * NCT; i += 256) {
+      const int tt = i / NCT, c = i % NCT;
+      const int t = t0 + tt;
+      gs[tt][c] = (t < t_end && c < NC) ? static_cast<A>(G[t * gst + c * gsc]) : A(0);
+    }
+    __syncthreads();
+    if (j < M) {
+      const int nt = min(32, t_end - t0);
+      for (int tt = 0; tt < nt; ++tt) {
+        const A xv = static_cast<A>(load_as_double<DT>(X, static_cast<long long>(t0 + tt) * M + j));
+#pragma unroll
+        for (int c = 0; c < NCT; ++c) acc[c] += xv * gs[tt][c];
+      }
+    }
+  }
+  if (j < M)
+#pragma unroll
+    for (int c = 0; c < NCT; ++c)
+      if (c < NC) part[(static_cast<long long>(chunk) * M + j) * NC + c] = static_cast<double>(acc[c]);
+}
+
+// dx[t][j] += sum_c G1(t,c) W1(j,c) [+ sum_c G2(t,c) W2(j,c)]: one pass over
+// dx for both projections of the noisy gate
+template <typename T, typename A, int NCT>
+__global__ void __launch_bounds__(256)
+    dx_acc2_kernel(int Tn, int M, int NC, const double* __restrict__ G1, const double* __restrict__ W1,
+                   const double* __restrict__ G2, const double* __restrict__ W2, long long gst,
+                   long long gsc, long long wsj, long long wsc, T* __restrict__ dx) {
+  __shared__ A gs[2][32][NCT];
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  const int t0 = blockIdx.y * 32;
+  const int npj = G2 ? 2 : 1;
+  A w1[NCT], w2[NCT];
+#pragma unroll
+  for (int c = 0; c < NCT; ++c) {
+    w1[c] = (j < M && c < NC) ? static_cast<A>(W1[j * wsj + c * wsc]) : A(0);
+    w2[c] = (j < M && c < NC && G2) ? static_cast<A>(W2[j * wsj + c * wsc]) : A(0);
+  }
+  for (int i = threadIdx.x; i < npj * 32 * NCT; i += 256) {
+    const int pj = i / (32 * NCT), tt = (i / NCT) % 32, c = i % NCT;
+    const double* G = pj ? G2 : G1;
+    gs[pj][tt][c] = (t0 + tt < Tn && c < NC) ? static_cast<A>(G[(t0 + tt) * gst + c * gsc]) : A(0);
+  }
+  __syncthreads();
+  if (j >= M) return;
+  for (int tt = 0; tt < 32 && t0 + tt < Tn; ++tt) {
+    A a = A(0);
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) a += gs[0][tt][c] * w1[c];
+    if (G2)
+#pragma unroll
+      for (int c = 0; c < NCT; ++c) a += gs[1][tt][c] * w2[c];
+    T* p = dx + static_cast<long long>(t0 + tt) * M + j;
+    if constexpr (sizeof(T) == 2) *p = __float2bfloat16(__bfloat162float(*p) + static_cast<float>(a));
+    else *p = static_cast<T>(static_cast<double>(*p) + static_cast<double>(a));
   }
 }
 
@@ -217,28 +298,77 @@ struct Ws {
   }
 };
 
+template <int NCT>
+void xtg2_launch(int xdt, int T, int M, int NC, const void* X, const double* G, long long gst,
+                 long long gsc, double* part, cudaStream_t st) {
+  dim3 grid((M + 255) / 256, (T + XT_TCH - 1) / XT_TCH);
+  switch (xdt) {
+    case FSMOE_F64: xtg2_kernel<0, double, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+    case FSMOE_F32: xtg2_kernel<1, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+    default: xtg2_kernel<2, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+  }
+  ::fsmoe::count_launch();
+}
+
 void xtg(int xdt, int T, int M, int NC, const void* X, const double* G, long long gst,
          long long gsc, double* out, long long osj, long long osc, int accumulate, double* part,
          cudaStream_t st) {
   const int nchunks = (T + XT_TCH - 1) / XT_TCH;
+  if (NC <= 64) {
+    if (NC <= 8) xtg2_launch<8>(xdt, T, M, NC, X, G, gst, gsc, part, st);
+    else if (NC <= 16) xtg2_launch<16>(xdt, T, M, NC, X, G, gst, gsc, part, st);
+    else if (NC <= 32) xtg2_launch<32>(xdt, T, M, NC, X, G, gst, gsc, part, st);
+    else xtg2_launch<64>(xdt, T, M, NC, X, G, gst, gsc, part, st);
+    long long n = static_cast<long long>(M) * NC;
+    xtg_reduce_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(nchunks, M, NC, part, out,
+                                                                         osj, osc, accumulate);
+    ::fsmoe::count_launch();
+    return;
+  }
   dim3 grid((M + XT_J - 1) / XT_J, (NC + XT_C - 1) / XT_C, nchunks);
   switch (xdt) {
-    case FSMOE_F64: xtg_partial_kernel<0><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
-    case FSMOE_F32: xtg_partial_kernel<1><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
-    default: xtg_partial_kernel<2><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
+    case FSMOE_F64: xtg_partial_kernel<0, double><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
+    case FSMOE_F32: xtg_partial_kernel<1, float><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
+    default: xtg_partial_kernel<2, float><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
   }
   long long n = static_cast<long long>(M) * NC;
   xtg_reduce_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(nchunks, M, NC, part, out,
                                                                        osj, osc, accumulate); ::fsmoe::count_launch();
 }
 
-void dx_acc(int xdt, int T, int M, int NC, const double* G, long long gst, long long gsc,
-            const double* W, long long wsj, long long wsc, void* dx, cudaStream_t st) {
+template <int NCT>
+void dx_acc2_launch(int xdt, int T, int M, int NC, const double* G1, const double* W1,
+                    const double* G2, const double* W2, long long gst, long long gsc, long long wsj,
+                    long long wsc, void* dx, cudaStream_t st) {
   dim3 grid((M + 255) / 256, (T + 31) / 32);
   switch (xdt) {
-    case FSMOE_F64: dx_acc_kernel<double><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<double*>(dx)); ::fsmoe::count_launch(); break;
-    case FSMOE_F32: dx_acc_kernel<float><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<float*>(dx)); ::fsmoe::count_launch(); break;
-    default: dx_acc_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<__nv_bfloat16*>(dx)); ::fsmoe::count_launch(); break;
+    case FSMOE_F64: dx_acc2_kernel<double, double, NCT><<<grid, 256, 0, st>>>(T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, static_cast<double*>(dx)); break;
+    case FSMOE_F32: dx_acc2_kernel<float, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, static_cast<float*>(dx)); break;
+    default: dx_acc2_kernel<__nv_bfloat16, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, static_cast<__nv_bfloat16*>(dx)); break;
+  }
+  ::fsmoe::count_launch();
+}
+
+// both projections at once when G2 != null (same strides)
+bool dx_acc_pair(int xdt, int T, int M, int NC, const double* G1, const double* W1,
+                 const double* G2, const double* W2, long long gst, long long gsc, long long wsj,
+                 long long wsc, void* dx, cudaStream_t st) {
+  if (NC > 64) return false;
+  if (NC <= 8) dx_acc2_launch<8>(xdt, T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, dx, st);
+  else if (NC <= 16) dx_acc2_launch<16>(xdt, T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, dx, st);
+  else if (NC <= 32) dx_acc2_launch<32>(xdt, T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, dx, st);
+  else dx_acc2_launch<64>(xdt, T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, dx, st);
+  return true;
+}
+
+void dx_acc(int xdt, int T, int M, int NC, const double* G, long long gst, long long gsc,
+            const double* W, long long wsj, long long wsc, void* dx, cudaStream_t st) {
+  if (dx_acc_pair(xdt, T, M, NC, G, W, nullptr, nullptr, gst, gsc, wsj, wsc, dx, st)) return;
+  dim3 grid((M + 255) / 256, (T + 31) / 32);
+  switch (xdt) {
+    case FSMOE_F64: dx_acc_kernel<double, double><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<double*>(dx)); ::fsmoe::count_launch(); break;
+    case FSMOE_F32: dx_acc_kernel<float, float><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<float*>(dx)); ::fsmoe::count_launch(); break;
+    default: dx_acc_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(T, M, NC, G, gst, gsc, W, wsj, wsc, static_cast<__nv_bfloat16*>(dx)); ::fsmoe::count_launch(); break;
   }
 }
 
@@ -279,8 +409,10 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ); ::fsmoe::count_launch();
       xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
       xtg(d.x_dtype, T, M, E, x, dZ, E, 1, dWn, E, 1, 1, part, st);
-      dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
-      dx_acc(d.x_dtype, T, M, E, dZ, E, 1, w_noise, E, 1, dx, st);
+      if (!dx_acc_pair(d.x_dtype, T, M, E, dS, w_score, dZ, w_noise, E, 1, E, 1, dx, st)) {
+        dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
+        dx_acc(d.x_dtype, T, M, E, dZ, E, 1, w_noise, E, 1, dx, st);
+      }
       break;
     }
     case FSMOE_GATE_SIGMOID_TOPK: {
