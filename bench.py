@@ -423,6 +423,19 @@ def gpu_arm(args):
             with open(f"{args.trace}.rank{rank}.json", "w") as f:
                 f.write(tj)
         timeline = timeline_summary(tj, nt)
+        if world > 1:
+            # every rank's exchange waits: a rank that waits long is waiting for
+            # a slower rank (expert load imbalance under capacity), the rank
+            # that waits least is on the critical path and its waits are the
+            # exchange latency the step really exposes
+            per = [None] * world
+            dist.all_gather_object(per, timeline["comm_exposed_ms_per_step"])
+            timeline["comm_wait_ms_per_step_by_rank"] = per
+            timeline["comm_exposed_ms_per_step"] = max(per)
+            timeline["exposed_alltoall_ms_per_step"] = min(per)
+            timeline["note"] = ("traced run synchronises per phase call; shares, not absolute step "
+                                "time. exposed_alltoall = the critical-path rank's exchange waits; "
+                                "larger waits on other ranks are expert-load imbalance")
 
     roof, gflops, gms = gemm_roofline(layer, peaks)
     roof["peak_source"] = peak_kind
