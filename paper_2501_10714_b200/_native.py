@@ -47,6 +47,19 @@ class GemmDesc(C.Structure):
     ]
 
 
+class PeerRows(C.Structure):
+    """fsmoe_peer_rows (include/fsmoe_cuda.h): where rows of a [P][E_l][C]
+    block buffer land (identity for one rank)."""
+    _fields_ = [("base", C.c_void_p * 8), ("world", C.c_int), ("rank", C.c_int),
+                ("experts_local", C.c_int), ("capacity", C.c_longlong)]
+
+
+class PeerFlags(C.Structure):
+    """fsmoe_peer_flags: per-rank uint64 arrival counters [nslots][world]."""
+    _fields_ = [("base", C.c_void_p * 8), ("world", C.c_int), ("rank", C.c_int),
+                ("nslots", C.c_int)]
+
+
 class GateDesc(C.Structure):
     _fields_ = [
         ("kind", C.c_int), ("top_k", C.c_int), ("seed", C.c_uint64), ("tokens", C.c_int),

@@ -170,6 +170,41 @@ def dispatch(x, pick_of_slot, pick_token, experts, capacity, chunks=1, out=None)
     return out
 
 
+def gather_rows(src, src_row, out=None):
+    """out[i] = src[src_row[i]] (src_row < 0: zero row), TMA row moves."""
+    lib = NL.cuda_lib()
+    n, M = src_row.numel(), src.shape[1]
+    if out is None:
+        out = torch.empty(n, M, dtype=src.dtype, device=src.device)
+    NL.check(lib.fsmoe_gather_rows(DTYPES[src.dtype], M, C.c_longlong(n), _i(src_row), _ptr(src),
+                                   _ptr(out), None, _stream()))
+    return out
+
+
+def peer_map(bases, rank, experts_local, capacity):
+    m = NL.PeerRows()
+    for i, b in enumerate(bases):
+        m.base[i] = b.data_ptr() if torch.is_tensor(b) else b
+    m.world, m.rank, m.experts_local, m.capacity = len(bases), rank, experts_local, capacity
+    return m
+
+
+def dispatch_peer(x, pick_of_slot, pick_token, experts, capacity, dst_map):
+    lib = NL.cuda_lib()
+    NL.check(lib.fsmoe_dispatch_peer(DTYPES[x.dtype], x.shape[1], experts, C.c_longlong(capacity),
+                                     _i(pick_of_slot), _i(pick_token), _ptr(x), C.byref(dst_map),
+                                     _stream()))
+
+
+def peer_signal(flags, slot):
+    NL.check(NL.cuda_lib().fsmoe_peer_signal(C.byref(flags), slot, None, C.c_longlong(0), None,
+                                             _stream()))
+
+
+def peer_wait(flags, slot, target):
+    NL.check(NL.cuda_lib().fsmoe_peer_wait(C.byref(flags), slot, C.c_ulonglong(target), _stream()))
+
+
 def combine(buffers, tok_ptr, tok_pick, slot_of_pick, pick_weight, tokens, experts, capacity,
             chunks=1, out=None):
     """I-Order: y[t] = sum_{kept picks} w * buffers[slot] (workload.cpp:266-282)."""
