@@ -214,6 +214,21 @@ int fsmoe_combine_bwd_peer(int dtype, int model_dim, int experts, long long capa
 int fsmoe_gather_rows(int dtype, int model_dim, long long n_rows, const int* src_row,
                       const void* src, void* dst, const fsmoe_peer_rows* dst_map, void* stream);
 
+/* The same over the slots [slot_lo, slot_hi) only (exclude = 0) or all but
+ * them (exclude = 1): the EP layer moves its own experts' rows first and the
+ * peers' rows on a second stream, overlapping the NVLink transfer with the
+ * expert GEMMs on the local rows. The range form of combine backward leaves
+ * d_weight of dropped picks alone (zero it before the first range call). */
+int fsmoe_dispatch_peer_range(int dtype, int model_dim, int experts, long long capacity,
+                              const int* pick_of_slot, const int* pick_token, const void* x,
+                              const fsmoe_peer_rows* dst, long long slot_lo, long long slot_hi,
+                              int exclude, void* stream);
+int fsmoe_combine_bwd_peer_range(int dtype, int model_dim, int experts, long long capacity,
+                                 long long n_picks, const int* pick_of_slot, const int* pick_token,
+                                 const double* pick_weight, const void* dy, const void* buffers,
+                                 const fsmoe_peer_rows* d_dst, double* d_weight, long long slot_lo,
+                                 long long slot_hi, int exclude, void* stream);
+
 typedef struct fsmoe_gemm_desc {
   int kind;        /* 0 row-grouped (fwd/dgrad), 1 k-grouped (wgrad) */
   int nblk, rows, K, N, Mo, No, n_w;
@@ -236,6 +251,12 @@ typedef struct fsmoe_gemm_desc {
   /* row-grouped epi 0/1 only: store output rows through this peer map
    * ([nblk][rows_total] rows, capacity = rows_total) instead of D */
   const fsmoe_peer_rows* d_peers;
+  /* row-grouped only: process blocks [blk_lo, blk_hi) (blk_exclude = 0) or
+   * all but them (1); blk_hi = 0 means every block */
+  int blk_lo, blk_hi, blk_exclude;
+  /* > 0: run the persistent grid on at most this many SMs (leaves the rest to
+   * a concurrent kernel, e.g. an NVLink row transfer); 0 = all */
+  int max_sms;
 } fsmoe_gemm_desc;
 
 int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream);

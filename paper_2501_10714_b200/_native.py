@@ -43,7 +43,8 @@ class GemmDesc(C.Structure):
         ("valid_rows", C.c_void_p), ("epi", C.c_int), ("D", C.c_void_p), ("D2", C.c_void_p),
         ("Zin", C.c_void_p), ("ldd", C.c_longlong), ("ldd2", C.c_longlong),
         ("ldz", C.c_longlong), ("accumulate", C.c_int), ("precision", C.c_int),
-        ("d_peers", C.c_void_p),
+        ("d_peers", C.c_void_p), ("blk_lo", C.c_int), ("blk_hi", C.c_int), ("blk_exclude", C.c_int),
+        ("max_sms", C.c_int),
     ]
 
 

@@ -176,6 +176,10 @@ struct MoELayer::Impl {
   // is exactly 1.0 (workload.cpp:123-133), so the I-order and its backward
   // are row gathers and the weight gradient is identically zero
   bool unit_top1 = false;
+  // EP with r = 1: move the local share first and the peers' share on s_aux,
+  // overlapping the NVLink transfer with GEMMs on the local blocks
+  bool split = false;
+  int split_sms = 0;
   bool peer = false;
   void* sym = nullptr;
   std::vector<void*> sym_peers;
@@ -193,8 +197,8 @@ struct MoELayer::Impl {
   int n_slots() const { return 4 + 2 * n_chunk_slots; }
 
   void peer_signal(int slot, const void* put = nullptr, long long put_row_bytes = 0,
-                   const fsmoe_peer_rows* put_map = nullptr) {
-    throw_on(fsmoe_peer_signal(&flags, slot, put, put_row_bytes, put_map, s_comp));
+                   const fsmoe_peer_rows* put_map = nullptr, cudaStream_t st = nullptr) {
+    throw_on(fsmoe_peer_signal(&flags, slot, put, put_row_bytes, put_map, st ? st : s_comp));
   }
   void peer_wait(int slot) {
     throw_on(fsmoe_peer_wait(&flags, slot, ++epoch[static_cast<size_t>(slot)], s_comp));
@@ -301,11 +305,25 @@ struct MoELayer::Impl {
     return d;
   }
 
-  void expert_fwd(const Chunk& c) {
+  // Blocks [rank*E_l, rank*E_l + E_l) of the [P][E_l][C] receive layout hold
+  // this rank's own tokens: they are local before any peer has delivered.
+  void local_blocks(fsmoe_gemm_desc& d, int exclude) const {
+    d.blk_lo = rank * El;
+    d.blk_hi = rank * El + El;
+    d.blk_exclude = exclude;
+    // the local-share GEMM runs beside the peers' NVLink row transfer: leave
+    // that kernel SMs of its own (the persistent GEMM otherwise fills them all)
+    if (!exclude) d.max_sms = split_sms;
+  }
+
+  // part 0: the whole expert forward; 1: GEMM1 on the local blocks only;
+  // 2: GEMM1 on the peers' blocks, then GEMM2 on everything
+  void expert_fwd(const Chunk& c, int part = 0) {
     const bool bf = cfg.precision == Precision::bf16;
     const bool gated = cfg.ffn == LayerConfig::Ffn::gated3;
     // GEMM1: Z = X W1^T (+ fused activation -> H)
     fsmoe_gemm_desc g1 = row_desc(c);
+    if (part) local_blocks(g1, part == 2);
     g1.K = M;
     g1.N = N1;
     g1.A = Xr;
@@ -324,6 +342,7 @@ struct MoELayer::Impl {
       throw_on(fsmoe_activation_f32(gated ? 3 : 2, P * El, static_cast<int>(C), c.lo, c.hi - c.lo, H,
                                     static_cast<const float*>(Z), nullptr,
                                     static_cast<float*>(Hh), s_comp));
+    if (part == 1) return;
     // GEMM2: O = H W2^T
     fsmoe_gemm_desc g2 = row_desc(c);
     g2.K = H;
@@ -337,9 +356,27 @@ struct MoELayer::Impl {
     gemm(g2);
   }
 
-  void expert_bwd(const Chunk& c, bool first) {
+  // part 0: the whole expert backward; 1: dgrad2 on the local blocks only
+  // (bf16: dZ over Z); 2: everything else (dgrad2 on the peers' blocks)
+  void expert_bwd(const Chunk& c, bool first, int part = 0) {
     const bool bf = cfg.precision == Precision::bf16;
     const bool gated = cfg.ffn == LayerConfig::Ffn::gated3;
+    if (part == 1) {
+      fsmoe_gemm_desc d2 = row_desc(c);
+      local_blocks(d2, 0);
+      d2.K = M;
+      d2.N = H;
+      d2.b_mn_major = 1;
+      d2.A = dOr;
+      d2.B = prm.w2;
+      d2.epi = gated ? 5 : 4;
+      d2.Zin = Z;
+      d2.ldz = N1;
+      d2.D = Z;
+      d2.ldd = N1;
+      gemm(d2);
+      return;
+    }
     // bf16: wgrad GEMMs on s_aux beside the dgrad GEMMs (independent inputs and
     // outputs); fp32 check mode writes dH over H, which wgrad2 reads: serial
     cudaStream_t sw = bf ? s_aux : s_comp;
@@ -369,6 +406,7 @@ struct MoELayer::Impl {
       d2.ldz = N1;
       d2.D = Z;
       d2.ldd = N1;
+      if (part == 2) local_blocks(d2, 1);
       gemm(d2);
     } else {
       d2.epi = 1;
@@ -581,6 +619,9 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   const long long rows = E * C;  // == P * E_l * C on both sides
   const long long ab = rows * M * I.esz;
   if (I.peer) {
+    const char* sp_env = std::getenv("FSMOE_EP_SPLIT");
+    I.split = I.fwd_chunks.size() == 1 && I.bwd_chunks.size() == 1 && sp_env && std::atoi(sp_env) > 0;
+    if (I.split) I.split_sms = std::atoi(sp_env) > 1 ? std::atoi(sp_env) : 0;
     I.n_chunk_slots = static_cast<int>(std::max(I.fwd_chunks.size(), I.bwd_chunks.size()));
     I.setup_peer(ab);
     I.Z = I.dalloc("Z", rows * I.N1 * I.esz);
@@ -647,7 +688,39 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
     throw_on(fsmoe_dispatch(I.dtype, I.M, I.E, I.C, 1, I.pos, I.tok, x, I.Xs, I.s_comp));
   I.tr.end(sp, I.s_comp);
   const auto& ch = I.fwd_chunks;
-  if (I.peer) {
+  if (I.peer && I.split) {
+    // order + dispatch AlltoAll in one kernel per share: this rank's own
+    // experts' rows first (local HBM), the peers' rows on s_aux over NVLink
+    // while GEMM1 already runs on the local blocks
+    const long long lo = static_cast<long long>(I.rank) * I.El * I.C, hi = lo + I.El * I.C;
+    sp = I.tr.begin("order-local", 2, I.s_comp);
+    I.peer_wait(I.slot_bar_fwd());
+    throw_on(fsmoe_dispatch_peer_range(I.dtype, I.M, I.E, I.C, I.pos, I.tok, x, &I.map_X, lo, hi, 0,
+                                       I.s_comp));
+    cuda_check(cudaMemcpyAsync(I.rfill + I.rank * I.El, I.fill + I.rank * I.El, 8 * I.El,
+                               cudaMemcpyDeviceToDevice, I.s_comp), "memcpy");
+    I.tr.end(sp, I.s_comp);
+    I.record(I.ev_x1, I.s_comp);
+    I.wait(I.s_aux, I.ev_x1);
+    throw_on(fsmoe_dispatch_peer_range(I.dtype, I.M, I.E, I.C, I.pos, I.tok, x, &I.map_X, lo, hi, 1,
+                                       I.s_aux));
+    I.peer_signal(I.slot_disp_fwd(), I.fill, 8, &I.map_fill, I.s_aux);
+    I.record(I.ev_x2, I.s_aux);
+    sp = I.tr.begin("expert-local", 2, I.s_comp);
+    I.expert_fwd(ch[0], 1);
+    I.tr.end(sp, I.s_comp);
+    sp = I.tr.begin("dispatch", 0, I.s_comp);
+    I.peer_wait(I.slot_disp_fwd());
+    I.wait(I.s_comp, I.ev_x2);
+    I.tr.end(sp, I.s_comp);
+    sp = I.tr.begin("expert[0]", 2, I.s_comp);
+    I.expert_fwd(ch[0], 2);
+    I.peer_signal(I.slot_comb_fwd(0));
+    I.tr.end(sp, I.s_comp);
+    sp = I.tr.begin("combine", 0, I.s_comp);
+    I.peer_wait(I.slot_comb_fwd(0));
+    I.tr.end(sp, I.s_comp);
+  } else if (I.peer) {
     // order + dispatch AlltoAll in one kernel: rows go straight to their owner
     sp = I.tr.begin("dispatch", 0, I.s_comp);
     I.peer_wait(I.slot_bar_fwd());
@@ -733,17 +806,49 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
       I.peer_wait(I.slot_bar_bwd());
     }
     // I-order backward fused with the dispatch AlltoAll of dO
-    sp = I.tr.begin("i-order", 2, I.s_comp);
-    if (I.unit_top1)  // dO[slot] = 1.0 * dy[token]; d_weight feeds no gradient (gate_bwd.cu)
-      throw_on(fsmoe_dispatch_peer(I.dtype, I.M, I.E, I.C, I.pos, I.tok, dy, &I.map_dO, I.s_comp));
-    else
-      throw_on(fsmoe_combine_bwd_peer(I.dtype, I.M, I.E, I.C, I.n_picks, I.pos, I.tok, I.w, dy, I.Os,
-                                      &I.map_dO, I.dw, I.s_comp));
-    I.tr.end(sp, I.s_comp);
-    sp = I.tr.begin("dispatch", 0, I.s_comp);
-    I.peer_signal(I.slot_disp_bwd());
-    I.peer_wait(I.slot_disp_bwd());
-    I.tr.end(sp, I.s_comp);
+    const bool split_bwd = I.split && cfg_.precision == Precision::bf16;
+    if (split_bwd) {
+      // own experts' dO rows first, the peers' rows on s_aux over NVLink while
+      // dgrad2 already runs on the local blocks
+      const long long lo = static_cast<long long>(I.rank) * I.El * I.C, hi = lo + I.El * I.C;
+      auto iorder = [&](int excl, cudaStream_t st_) {
+        if (I.unit_top1)  // dO[slot] = 1.0 * dy[token]; d_weight feeds no gradient (gate_bwd.cu)
+          throw_on(fsmoe_dispatch_peer_range(I.dtype, I.M, I.E, I.C, I.pos, I.tok, dy, &I.map_dO, lo,
+                                             hi, excl, st_));
+        else
+          throw_on(fsmoe_combine_bwd_peer_range(I.dtype, I.M, I.E, I.C, I.n_picks, I.pos, I.tok, I.w,
+                                                dy, I.Os, &I.map_dO, I.dw, lo, hi, excl, st_));
+      };
+      sp = I.tr.begin("i-order", 2, I.s_comp);
+      if (!I.unit_top1)
+        cuda_check(cudaMemsetAsync(I.dw, 0, 8 * I.n_picks, I.s_comp), "memset");
+      iorder(0, I.s_comp);
+      I.tr.end(sp, I.s_comp);
+      I.record(I.ev_x1, I.s_comp);
+      I.wait(I.s_aux, I.ev_x1);
+      iorder(1, I.s_aux);
+      I.peer_signal(I.slot_disp_bwd(), nullptr, 0, nullptr, I.s_aux);
+      I.record(I.ev_x2, I.s_aux);
+      sp = I.tr.begin("expert-local", 2, I.s_comp);
+      I.expert_bwd(ch[0], true, 1);
+      I.tr.end(sp, I.s_comp);
+      sp = I.tr.begin("dispatch", 0, I.s_comp);
+      I.peer_wait(I.slot_disp_bwd());
+      I.wait(I.s_comp, I.ev_x2);
+      I.tr.end(sp, I.s_comp);
+    } else {
+      sp = I.tr.begin("i-order", 2, I.s_comp);
+      if (I.unit_top1)  // dO[slot] = 1.0 * dy[token]; d_weight feeds no gradient (gate_bwd.cu)
+        throw_on(fsmoe_dispatch_peer(I.dtype, I.M, I.E, I.C, I.pos, I.tok, dy, &I.map_dO, I.s_comp));
+      else
+        throw_on(fsmoe_combine_bwd_peer(I.dtype, I.M, I.E, I.C, I.n_picks, I.pos, I.tok, I.w, dy,
+                                        I.Os, &I.map_dO, I.dw, I.s_comp));
+      I.tr.end(sp, I.s_comp);
+      sp = I.tr.begin("dispatch", 0, I.s_comp);
+      I.peer_signal(I.slot_disp_bwd());
+      I.peer_wait(I.slot_disp_bwd());
+      I.tr.end(sp, I.s_comp);
+    }
     if (I.prm.dense_grad && cfg_.dense_grad_elems > 0) {
       // gradient allreduce slices on the comm stream, overlapping expert backward
       I.record(I.ev_gate, I.s_comp);
@@ -756,7 +861,7 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
     for (size_t j = 0; j < ch.size(); ++j) {
       // dgrad1's epilogue stores the combine AlltoAll into the owners' dX_send
       sp = I.tr.begin("expert[" + std::to_string(j) + "]", 2, I.s_comp);
-      I.expert_bwd(ch[j], j == 0);
+      I.expert_bwd(ch[j], j == 0, split_bwd ? 2 : 0);
       I.peer_signal(I.slot_comb_bwd(j));
       I.tr.end(sp, I.s_comp);
     }

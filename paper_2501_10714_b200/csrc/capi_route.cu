@@ -166,6 +166,30 @@ int fsmoe_dispatch_peer(int dtype, int model_dim, int experts, long long capacit
                          peer_rows_of(dst), as_stream(stream));
 }
 
+int fsmoe_dispatch_peer_range(int dtype, int model_dim, int experts, long long capacity,
+                              const int* pick_of_slot, const int* pick_token, const void* x,
+                              const fsmoe_peer_rows* dst, long long slot_lo, long long slot_hi,
+                              int exclude, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (capacity <= 0) return config_error("dispatch: capacity must be positive");
+  if (int rc = check_peer_map(dst, experts, capacity)) return rc;
+  return dispatch_launch(dtype, model_dim, experts, capacity, 1, pick_of_slot, pick_token, x,
+                         peer_rows_of(dst), as_stream(stream),
+                         fsmoe_dev::RowRange{slot_lo, slot_hi, exclude});
+}
+
+int fsmoe_combine_bwd_peer_range(int dtype, int model_dim, int experts, long long capacity,
+                                 long long n_picks, const int* pick_of_slot, const int* pick_token,
+                                 const double* pick_weight, const void* dy, const void* buffers,
+                                 const fsmoe_peer_rows* d_dst, double* d_weight, long long slot_lo,
+                                 long long slot_hi, int exclude, void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (int rc = check_peer_map(d_dst, experts, capacity)) return rc;
+  return combine_bwd_launch(dtype, model_dim, experts, capacity, 1, n_picks, pick_of_slot,
+                            pick_token, pick_weight, dy, buffers, peer_rows_of(d_dst), d_weight,
+                            as_stream(stream), fsmoe_dev::RowRange{slot_lo, slot_hi, exclude});
+}
+
 int fsmoe_combine_bwd_peer(int dtype, int model_dim, int experts, long long capacity,
                            long long n_picks, const int* pick_of_slot, const int* pick_token,
                            const double* pick_weight, const void* dy, const void* buffers,

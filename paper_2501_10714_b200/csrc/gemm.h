@@ -71,6 +71,8 @@ struct GemmProblem {
   // through this peer map (NVLink stores into the owning rank) instead of D.
   bool use_peers = false;
   fsmoe_dev::PeerRows peers{};
+  fsmoe_dev::RowRange blocks = fsmoe_dev::all_rows();  // row-grouped: blocks processed
+  int max_sms = 0;                                        // > 0: cap the persistent grid
 };
 
 // bf16 operands, fp32 accumulate in TMEM (tcgen05). Returns cudaError_t.

@@ -21,6 +21,7 @@ struct SParams {
   int accumulate;
   int use_peers;
   fsmoe_dev::PeerRows peers;
+  fsmoe_dev::RowRange blocks;
 };
 
 __device__ __forceinline__ int valid_rows(const SParams& p, int b) {
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SParams p) {
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int out_rows = p.kind == 0 ? p.rows : p.Mo;
   const int out_cols = p.kind == 0 ? p.N : p.No;
-  if (p.kind == 0 && m0 >= valid_rows(p, g)) return;
+  if (p.kind == 0 && (m0 >= valid_rows(p, g) || !fsmoe_dev::in_range(p.blocks, g))) return;
   float acc[4][4] = {};
 
   auto tile = [&](auto loadA, auto loadB, int klen) {
@@ -139,6 +140,7 @@ int gemm_simt_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.accumulate = pr.accumulate ? 1 : 0;
   p.use_peers = pr.use_peers ? 1 : 0;
   p.peers = pr.peers;
+  p.blocks = pr.blocks;
   dim3 grid;
   if (pr.kind == GemmKind::RowGrouped) {
     grid = dim3((pr.N + TN - 1) / TN, (pr.rows + TM - 1) / TM, pr.nblk);

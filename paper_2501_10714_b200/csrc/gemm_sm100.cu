@@ -51,6 +51,7 @@ struct KParams {
   int out_rows, out_cols;  // valid output extent per group
   int use_peers;           // row-grouped plain stores through `peers`
   fsmoe_dev::PeerRows peers;
+  fsmoe_dev::RowRange blocks;  // row-grouped: the blocks this launch covers
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -235,7 +236,8 @@ __device__ __forceinline__ TileInfo decode_tile_c(const KParams& p, int t) {
   int rem = t - ti.g * per_g;
   ti.mt = rem / p.n_tiles;
   ti.nt = rem - ti.mt * p.n_tiles;
-  ti.skip = p.kind == 0 && ti.mt * TileCfg<CTAS>::BM >= valid_of(p, ti.g);
+  ti.skip = p.kind == 0 &&
+            (ti.mt * TileCfg<CTAS>::BM >= valid_of(p, ti.g) || !fsmoe_dev::in_range(p.blocks, ti.g));
   return ti;
 }
 
@@ -750,6 +752,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.accumulate = pr.accumulate ? 1 : 0;
   p.use_peers = pr.use_peers ? 1 : 0;
   p.peers = pr.peers;
+  p.blocks = pr.blocks;
   p.rows_total = pr.rows_total > 0 ? pr.rows_total : pr.rows;
   p.row0 = pr.row0;
   if (pr.nblk <= 0 || pr.rows <= 0) return cudaSuccess;
@@ -836,7 +839,8 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
       }
     }
   }
-  const int max_units = num_sms() / ctas;
+  const int sms = pr.max_sms > 0 && pr.max_sms < num_sms() ? pr.max_sms : num_sms();
+  const int max_units = sms / ctas > 0 ? sms / ctas : 1;
   const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
   static bool smem_set[2][2] = {{false, false}, {false, false}};
   auto launch = [&](auto kern, int smem) -> cudaError_t {

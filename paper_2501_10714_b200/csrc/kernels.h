@@ -61,7 +61,8 @@ int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, in
                        void* ws, cudaStream_t st);
 
 int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int* pick_of_slot,
-                    const int* ptok, const void* x, const fsmoe_dev::PeerRows& buf, cudaStream_t st);
+                    const int* ptok, const void* x, const fsmoe_dev::PeerRows& buf, cudaStream_t st,
+                    const fsmoe_dev::RowRange& rr = fsmoe_dev::all_rows());
 int combine_launch(int dtype, int T, int M, int E, long long C, int chunks, const int* tptr,
                    const int* tpick, const int* slot_of_pick, const double* pw, const void* buf,
                    void* y, cudaStream_t st);
@@ -73,6 +74,6 @@ int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, co
 int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long long P,
                        const int* pick_of_slot, const int* ptok, const double* pw,
                        const void* dy, const void* buf, const fsmoe_dev::PeerRows& dbuf, double* dw,
-                       cudaStream_t st);
+                       cudaStream_t st, const fsmoe_dev::RowRange& rr = fsmoe_dev::all_rows());
 
 }  // namespace fsmoe

@@ -206,9 +206,9 @@ template <typename V>
 __global__ void __launch_bounds__(256)
     dispatch_kernel(long long n_slots, int row_vecs, int E, long long C, int chunks,
                     const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
-                    const V* __restrict__ x, const PeerRows buf) {
+                    const V* __restrict__ x, const PeerRows buf, const RowRange rr) {
   const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
-  if (s >= n_slots) return;
+  if (s >= n_slots || !in_range(rr, s)) return;
   const int lane = threadIdx.x & 31;
   const int p = pick_of_slot[s];
   V* dst = reinterpret_cast<V*>(
@@ -239,7 +239,7 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
 __global__ void __launch_bounds__(32)
     dispatch_bulk_kernel(long long n_slots, int row_bytes, int E, long long C, int chunks,
                          const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
-                         const uint8_t* __restrict__ x, const PeerRows buf) {
+                         const uint8_t* __restrict__ x, const PeerRows buf, const RowRange rr) {
   extern __shared__ __align__(128) uint8_t sm[];  // [BK_ROWS][row_bytes] + one zero row
   __shared__ __align__(8) uint64_t bar;
   const int lane = threadIdx.x;
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(32)
   }
   __syncwarp();
   int p = -1;
-  const bool valid = s < n_slots;
+  const bool valid = s < n_slots && in_range(rr, s);
   if (valid) p = pick_of_slot[s];
   uint8_t* mine = sm + lane * row_bytes;
   if (p >= 0) {
@@ -548,10 +548,11 @@ __global__ void __launch_bounds__(256)
     combine_bwd_kernel(long long n_slots, int M, int E, long long C, int chunks,
                        const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
                        const double* __restrict__ pw, const T* __restrict__ dy,
-                       const T* __restrict__ buf, const PeerRows dbuf, double* __restrict__ dw) {
+                       const T* __restrict__ buf, const PeerRows dbuf, double* __restrict__ dw,
+                       const RowRange rr) {
   using A = typename Acc<T>::type;
   const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
-  if (s >= n_slots) return;
+  if (s >= n_slots || !in_range(rr, s)) return;
   const int lane = threadIdx.x & 31;
   const int p = pick_of_slot[s];
   const long long row = slot_row(s, E, C, chunks);
@@ -675,7 +676,8 @@ int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, co
 }
 
 int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int* pick_of_slot,
-                    const int* ptok, const void* x, const PeerRows& buf, cudaStream_t st) {
+                    const int* ptok, const void* x, const PeerRows& buf, cudaStream_t st,
+                    const RowRange& rr) {
   const long long n_slots = static_cast<long long>(E) * C;
   if (n_slots <= 0 || M <= 0) return FSMOE_OK;
   const long long row_bytes = static_cast<long long>(M) * elem_size(dtype);
@@ -689,20 +691,20 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
     }
     dispatch_bulk_kernel<<<static_cast<int>((n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
         n_slots, static_cast<int>(row_bytes), E, C, chunks, pick_of_slot, ptok,
-        static_cast<const uint8_t*>(x), buf);
+        static_cast<const uint8_t*>(x), buf, rr);
     ::fsmoe::count_launch();
   } else if (row_bytes % 16 == 0) {
     dispatch_kernel<uint4><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 16), E, C,
                                                  chunks, pick_of_slot, ptok,
-                                                 static_cast<const uint4*>(x), buf); ::fsmoe::count_launch();
+                                                 static_cast<const uint4*>(x), buf, rr); ::fsmoe::count_launch();
   } else if (row_bytes % 8 == 0) {
     dispatch_kernel<uint2><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 8), E, C,
                                                  chunks, pick_of_slot, ptok,
-                                                 static_cast<const uint2*>(x), buf); ::fsmoe::count_launch();
+                                                 static_cast<const uint2*>(x), buf, rr); ::fsmoe::count_launch();
   } else {
     dispatch_kernel<uint16_t><<<grid, 256, 0, st>>>(
         n_slots, static_cast<int>(row_bytes / 2), E, C, chunks, pick_of_slot, ptok,
-        static_cast<const uint16_t*>(x), buf); ::fsmoe::count_launch();
+        static_cast<const uint16_t*>(x), buf, rr); ::fsmoe::count_launch();
   }
   return cuda_status(cudaGetLastError(), "fsmoe_dispatch");
 }
@@ -750,9 +752,11 @@ int dispatch_bwd_launch(int dtype, int T, int M, int E, long long C, int chunks,
 int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long long P,
                        const int* pick_of_slot, const int* ptok, const double* pw,
                        const void* dy, const void* buf, const PeerRows& dbuf, double* dw,
-                       cudaStream_t st) {
+                       cudaStream_t st, const RowRange& rr) {
   const long long n_slots = static_cast<long long>(E) * C;
-  if (P > 0) FSMOE_CUDA_TRY(cudaMemsetAsync(dw, 0, sizeof(double) * P, st), "combine_bwd memset");
+  // (a range launch leaves dw of the other slots' picks alone)
+  if (P > 0 && !rr.excl && rr.lo <= 0 && rr.hi >= static_cast<long long>(E) * C)
+    FSMOE_CUDA_TRY(cudaMemsetAsync(dw, 0, sizeof(double) * P, st), "combine_bwd memset");
   if (n_slots <= 0 || M <= 0) return FSMOE_OK;
   const int grid = static_cast<int>((n_slots + 7) / 8);
   int rc = by_dtype(dtype, [&](auto tag) {
@@ -761,12 +765,12 @@ int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long lo
       combine_bwd_kernel<Tt, true><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
                                                          static_cast<const Tt*>(dy),
                                                          static_cast<const Tt*>(buf),
-                                                         dbuf, dw);
+                                                         dbuf, dw, rr);
     else
       combine_bwd_kernel<Tt, false><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
                                                           static_cast<const Tt*>(dy),
                                                           static_cast<const Tt*>(buf),
-                                                          dbuf, dw);
+                                                          dbuf, dw, rr);
     ::fsmoe::count_launch();
   });
   if (rc) return config_error("combine_bwd: unknown dtype");

@@ -64,6 +64,18 @@ __device__ __forceinline__ char* peer_row(const PeerRows& m, long long row, long
   return m.base[p] + ((static_cast<long long>(m.rank) * m.el + e) * m.cap + c) * row_bytes;
 }
 
+// Which rows / slots / blocks a launch covers: [lo, hi), or everything but
+// that range when excl. Lets the EP layer run its local share of a
+// permutation or GEMM first and the peers' share on a second stream.
+struct RowRange {
+  long long lo, hi;
+  int excl;
+};
+__host__ __device__ __forceinline__ bool in_range(const RowRange& r, long long i) {
+  return (i >= r.lo && i < r.hi) != (r.excl != 0);
+}
+__host__ __device__ __forceinline__ RowRange all_rows() { return RowRange{0, (1LL << 62), 0}; }
+
 // Monotone map double -> uint64 (a < b  <=>  key(a) < key(b)) for non-NaN.
 __device__ __forceinline__ uint64_t order_key(double v) {
   if (v == 0.0) v = 0.0;  // -0.0 == +0.0 in the reference's comparisons
