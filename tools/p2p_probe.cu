@@ -192,5 +192,44 @@ int main() {
              bytes / (ms0 / 20 * 1e-3) / 1e9, bytes / (ms1 / 20 * 1e-3) / 1e9);
     }
   }
+  // copy engines: one large cudaMemcpyAsync into the peer's buffer (no SMs)
+  for (int rep = 0; rep < 2; ++rep) {
+    CK(cudaSetDevice(0));
+    for (int w = 0; w < 3; ++w) CK(cudaMemcpyAsync(dpeer, src, bytes, cudaMemcpyDeviceToDevice, 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(a, 0));
+    for (int r = 0; r < 20; ++r) CK(cudaMemcpyAsync(dpeer, src, bytes, cudaMemcpyDeviceToDevice, 0));
+    CK(cudaEventRecord(b, 0));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    printf("copy engine peer 16 MB: %7.1f GB/s\n", bytes / (ms / 20 * 1e-3) / 1e9);
+  }
+  // both directions at once
+  CK(cudaSetDevice(0));
+  CK(cudaEventRecord(a, 0));
+  CK(cudaSetDevice(1));
+  CK(cudaEventRecord(a1, s1));
+  for (int r = 0; r < 20; ++r) {
+    CK(cudaSetDevice(0));
+    CK(cudaMemcpyAsync(dpeer, src, bytes, cudaMemcpyDeviceToDevice, 0));
+    CK(cudaSetDevice(1));
+    CK(cudaMemcpyAsync(dpeer0, src1, bytes, cudaMemcpyDeviceToDevice, s1));
+  }
+  CK(cudaSetDevice(0));
+  CK(cudaEventRecord(b, 0));
+  CK(cudaSetDevice(1));
+  CK(cudaEventRecord(b1, s1));
+  CK(cudaEventSynchronize(b1));
+  CK(cudaSetDevice(0));
+  CK(cudaEventSynchronize(b));
+  {
+    float ms0 = 0, ms1 = 0;
+    CK(cudaEventElapsedTime(&ms0, a, b));
+    CK(cudaSetDevice(1));
+    CK(cudaEventElapsedTime(&ms1, a1, b1));
+    printf("copy engine bidir: gpu0 %7.1f GB/s gpu1 %7.1f GB/s\n", bytes / (ms0 / 20 * 1e-3) / 1e9,
+           bytes / (ms1 / 20 * 1e-3) / 1e9);
+  }
   return 0;
 }
