@@ -465,9 +465,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       auto release_acc = [&]() {
         tc_fence_before();
         __syncwarp();
+        // the tcgen05 fence orders this warp's (completed) TMEM reads before
+        // the hand-off; nothing else needs ordering, so the arrive is relaxed
+        // (a release arrive costs a MEMBAR + ERRBAR per warp per tile)
         if (lane == 0) {
-          if constexpr (CTAS == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
-          else mbar_arrive(&tempty_bar[acc]);
+          if constexpr (CTAS == 2) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+          else mbar_arrive_relaxed(&tempty_bar[acc]);
         }
         released = true;
       };
