@@ -34,6 +34,7 @@ using namespace fsmoe_dev;
 constexpr int AS_THREADS = 1024;
 constexpr int AS_TILE = AS_THREADS;  // picks per tile (one round per block)
 constexpr int AS_MAX_E = 256;
+constexpr int AS_CNT_CACHE = 2048;  // tile histograms kept in shared memory (ints)
 
 // cnt[tile][e] = picks of expert e inside the tile; flags bad picks.
 __global__ void __launch_bounds__(AS_THREADS)
@@ -64,26 +65,34 @@ __global__ void __launch_bounds__(AS_THREADS)
                        long long* __restrict__ dropped) {
   __shared__ int base[AS_MAX_E];
   __shared__ int wc[AS_THREADS / 32][AS_MAX_E];
+  __shared__ int cs[AS_CNT_CACHE];
+  __shared__ long long drop_acc;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // every tile's histogram in one parallel load (not a dependent load per
+  // tile), then per-expert prefix / totals from shared memory
+  const int ncnt = ntiles * E;
+  const bool cached = ncnt <= AS_CNT_CACHE;
+  if (cached)
+    for (int i = threadIdx.x; i < ncnt; i += AS_THREADS) cs[i] = cnt[i];
+  if (threadIdx.x == 0) drop_acc = 0;
+  __syncthreads();
   for (int e = threadIdx.x; e < E; e += AS_THREADS) {
     int b = 0;
-    for (int tl = 0; tl < static_cast<int>(blockIdx.x); ++tl) b += cnt[tl * E + e];
+    long long tot = 0;
+    for (int tl = 0; tl < ntiles; ++tl) {
+      const int v = cached ? cs[tl * E + e] : cnt[tl * E + e];
+      if (tl < static_cast<int>(blockIdx.x)) b += v;
+      tot += v;
+    }
     base[e] = b;
     if (blockIdx.x == 0) {
-      long long tot = 0;
-      for (int tl = 0; tl < ntiles; ++tl) tot += cnt[tl * E + e];
       fill[e] = tot < C ? tot : C;
+      if (tot > C) atomicAdd(reinterpret_cast<unsigned long long*>(&drop_acc),
+                             static_cast<unsigned long long>(tot - C));
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    long long d = 0;
-    for (int e = 0; e < E; ++e) {
-      long long tot = 0;
-      for (int tl = 0; tl < ntiles; ++tl) tot += cnt[tl * E + e];
-      d += tot > C ? tot - C : 0;
-    }
-    *dropped = d;
-  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *dropped = drop_acc;
   const long long tile0 = static_cast<long long>(blockIdx.x) * AS_TILE;
   for (int r = 0; r < AS_TILE / AS_THREADS; ++r) {
     for (int i = threadIdx.x; i < (AS_THREADS / 32) * E; i += AS_THREADS) wc[i / E][i % E] = 0;
