@@ -355,28 +355,32 @@ def gpu_arm(args):
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
         dyh = dy.cpu().pin_memory()
-        dxh = [torch.empty_like(xh).pin_memory() for _ in range(2)]
-        xd = [torch.empty_like(x) for _ in range(2)]
-        dyd = [torch.empty_like(dy) for _ in range(2)]
-        dxd = [torch.empty_like(dx) for _ in range(2)]
+        NB = 3  # triple-buffered: step i+1's H2D never waits on step i-1's D2H
+        dxh = [torch.empty_like(xh).pin_memory() for _ in range(NB)]
+        xd = [torch.empty_like(x) for _ in range(NB)]
+        dyd = [torch.empty_like(dy) for _ in range(NB)]
+        dxd = [torch.empty_like(dx) for _ in range(NB)]
         comp = torch.cuda.current_stream()
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_done = [torch.cuda.Event() for _ in range(2)]
-        ev_free = [torch.cuda.Event() for _ in range(2)]
-        for i in range(2):
+        ev_x = [torch.cuda.Event() for _ in range(NB)]
+        ev_dy = [torch.cuda.Event() for _ in range(NB)]
+        ev_done = [torch.cuda.Event() for _ in range(NB)]
+        ev_free = [torch.cuda.Event() for _ in range(NB)]
+        for i in range(NB):
             ev_free[i].record(comp)
 
         def e2e_steps(n):
             for i in range(n):
-                b = i % 2
+                b = i % NB
                 with torch.cuda.stream(s_in):
-                    s_in.wait_event(ev_free[b])       # step i-2 no longer reads set b
+                    s_in.wait_event(ev_free[b])       # step i-NB no longer uses set b
                     xd[b].copy_(xh, non_blocking=True)
+                    ev_x[b].record(s_in)
                     dyd[b].copy_(dyh, non_blocking=True)
-                    ev_in[b].record(s_in)
-                comp.wait_event(ev_in[b])
+                    ev_dy[b].record(s_in)
+                comp.wait_event(ev_x[b])              # forward needs x only
                 layer.forward(xd[b], y)
+                comp.wait_event(ev_dy[b])
                 layer.backward(dyd[b], dxd[b])
                 ev_done[b].record(comp)
                 with torch.cuda.stream(s_out):
@@ -386,7 +390,7 @@ def gpu_arm(args):
             comp.wait_stream(s_out)
 
         ke = max(1, min(args.steps, 50))
-        e2e_steps(2)
+        e2e_steps(NB)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -403,7 +407,7 @@ def gpu_arm(args):
                "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
                "d2h_bytes_per_step": dx.numel() * dx.element_size(), "ms_per_step": ems,
                "api": "paper_2501_10714_b200.layer.MoELayer forward+backward (libfsmoe.so C ABI)",
-               "copies": "pinned host buffers, H2D/D2H on copy streams double-buffered "
+               "copies": "pinned host buffers, H2D/D2H on copy streams triple-buffered "
                          "against compute, all inside the timed region"}
 
     timeline = None
