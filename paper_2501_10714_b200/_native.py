@@ -31,6 +31,10 @@ class ConfigError(NativeError):
     """Mirror of fsmoe::ConfigError (common.hpp:16-18), status 2."""
 
 
+class FitQualityError(NativeError):
+    """Mirror of fsmoe::FitQualityError (common.hpp:22-24), status 3."""
+
+
 class InvariantError(NativeError):
     """Mirror of fsmoe::InvariantError (common.hpp:26-28), status 4."""
 
@@ -103,6 +107,8 @@ def check(rc: int, lib: C.CDLL | None = None) -> None:
     msg = (fn() or b"").decode()
     if rc == 2:
         raise ConfigError(rc, msg)
+    if rc == 3:
+        raise FitQualityError(rc, msg)
     if rc == 4:
         raise InvariantError(rc, msg)
     raise NativeError(rc, msg or f"native status {rc}")
