@@ -147,6 +147,8 @@ def collect(cfg, world: int, reps=10):
     sizes = [a2a / 8, a2a / 4, a2a / 2, a2a]
     cap = int(vol[6])
     caps = sorted({max(128, (cap // d) // 128 * 128) for d in (8, 4, 2, 1)})
+    while len(caps) < 3:          # small capacities: the fit still needs a slope
+        caps.append(caps[-1] * 2)
     return profile_collectives(sizes, reps=reps) + profile_gemm(cfg.experts, caps, cfg.model_dim,
                                                                 cfg.ffn_dim, reps=reps), vol
 
