@@ -25,7 +25,7 @@
     }                                                                          \
   } while (0)
 
-constexpr int STAGES = 8;
+constexpr int MAX_STAGES = 13;
 constexpr int BOX_ROWS = 128;
 constexpr int BOX_BYTES = BOX_ROWS * 128;
 
@@ -65,11 +65,13 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(64) probe(const __grid_constant__ CUtensorMap map, int mode,
-                                            int iters, int ntiles) {
+__device__ unsigned long long g_clk[2];
+
+__global__ void __launch_bounds__(160) probe(const __grid_constant__ CUtensorMap map, int mode,
+                                            int iters, int ntiles, int STAGES, const uint8_t* raw) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint64_t full[MAX_STAGES], empty[MAX_STAGES];
   const uint32_t cs = nctarank(), rank = ctarank();
   const int cluster = blockIdx.x / cs;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -81,8 +83,13 @@ __global__ void __launch_bounds__(64) probe(const __grid_constant__ CUtensorMap 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster_sync();
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < iters; ++i) {
+  unsigned long long c0 = clock64(), t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  // producers: warp 0 (+ warps 2.. for modes 5 / 6: 2 / 4 issuing threads)
+  const int nprod = mode == 5 ? 2 : mode == 6 ? 4 : 1;
+  const int pidx = warp == 0 ? 0 : warp - 1;
+  if (warp != 1 && pidx < nprod && lane == 0) {
+    for (int i = pidx; i < iters; i += nprod) {
       const int s = i % STAGES;
       if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
       mbar_expect(&full[s], BOX_BYTES);
@@ -100,6 +107,20 @@ __global__ void __launch_bounds__(64) probe(const __grid_constant__ CUtensorMap 
             "l"(reinterpret_cast<uint64_t>(&map)), "r"(su32(&full[s])), "r"(0),
             "r"(static_cast<int>(rank) * rows), "r"(tile), "h"(mask)
             : "memory");
+      } else if (mode == 3) {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                su32(dst)),
+            "l"(raw + static_cast<size_t>(tile) * BOX_BYTES), "r"(BOX_BYTES), "r"(su32(&full[s]))
+            : "memory");
+      } else if (mode == 4) {
+        for (int part = 0; part < 2; ++part)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst + part * BOX_BYTES / 2)),
+              "l"(reinterpret_cast<uint64_t>(&map)), "r"(su32(&full[s])), "r"(0), "r"(part * BOX_ROWS / 2),
+              "r"(tile)
+              : "memory");
       } else {
         for (int part = 0; part < 1; ++part)
           asm volatile(
@@ -121,6 +142,12 @@ __global__ void __launch_bounds__(64) probe(const __grid_constant__ CUtensorMap 
     }
   }
   cluster_sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_clk[0] = clock64() - c0;
+    g_clk[1] = t1 - t0;
+  }
 }
 
 int main(int argc, char** argv) {
@@ -137,13 +164,18 @@ int main(int argc, char** argv) {
   cuuint64_t dims[3] = {64, BOX_ROWS, static_cast<cuuint64_t>(ntiles)};
   cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(BOX_BYTES)};
   const int iters = 20000;
-  const int smem = STAGES * BOX_BYTES + 1024;
+  const int smem = MAX_STAGES * BOX_BYTES + 1024;
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const int only_uc = argc > 2;
+  for (int stages : {4, 8, 13})
   for (int cs : {1, 2, 4, 8}) {
-    for (int mode = 0; mode < 3; ++mode) {
-      if (cs == 1 && mode > 0) continue;
-      cuuint32_t box[3] = {64, static_cast<cuuint32_t>(mode == 2 ? BOX_ROWS / cs : BOX_ROWS), 1};
+    for (int mode = 0; mode < 7; ++mode) {
+      if (cs == 1 && (mode == 1 || mode == 2)) continue;
+      if (cs > 1 && mode > 2) continue;
+      if (only_uc && (cs > 1 || mode == 1 || mode == 2)) continue;
+      if (!only_uc && stages != 8) continue;
+      cuuint32_t box[3] = {64, static_cast<cuuint32_t>(mode == 2 ? BOX_ROWS / cs : mode == 4 ? BOX_ROWS / 2 : BOX_ROWS), 1};
       cuuint32_t es[3] = {1, 1, 1};
       CUresult r = cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es,
                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -160,7 +192,7 @@ int main(int argc, char** argv) {
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cfg.blockDim = dim3(64);
+      cfg.blockDim = dim3(160);
       cfg.dynamicSmemBytes = smem;
       int max_clusters = 0;
       cfg.gridDim = dim3(cs * 64);
@@ -170,9 +202,9 @@ int main(int argc, char** argv) {
       cudaEvent_t a, b;
       CK(cudaEventCreate(&a));
       CK(cudaEventCreate(&b));
-      CK(cudaLaunchKernelEx(&cfg, probe, map, mode, 200, ntiles));
+      CK(cudaLaunchKernelEx(&cfg, probe, map, mode, 200, ntiles, stages, (const uint8_t*)buf));
       CK(cudaEventRecord(a));
-      CK(cudaLaunchKernelEx(&cfg, probe, map, mode, iters, ntiles));
+      CK(cudaLaunchKernelEx(&cfg, probe, map, mode, iters, ntiles, stages, (const uint8_t*)buf));
       CK(cudaEventRecord(b));
       CK(cudaEventSynchronize(b));
       CK(cudaGetLastError());
@@ -180,8 +212,12 @@ int main(int argc, char** argv) {
       CK(cudaEventElapsedTime(&ms, a, b));
       const double delivered = static_cast<double>(grid) * iters * BOX_BYTES;
       const double l2_reads = mode == 1 ? delivered : delivered / (mode == 2 ? 1.0 : 1.0);
-      printf("cluster %d mode %s: grid %d (max clusters %d), delivered %.2f TB/s (%.1f GB/s per SM)\n", cs,
-             mode == 0 ? "UC-distinct" : mode == 1 ? "UC-same    " : "MC         ", grid, max_clusters,
+      unsigned long long clk[2];
+      CK(cudaMemcpyFromSymbol(clk, g_clk, sizeof(clk)));
+      const double ghz = static_cast<double>(clk[0]) / clk[1];
+      printf("%.3f GHz, %.1f B/clk/SM | ", ghz, delivered / grid / (ms * 1e-3) / (ghz * 1e9));
+      printf("stages %d cluster %d mode %s: grid %d (max clusters %d), delivered %.2f TB/s (%.1f GB/s per SM)\n", stages, cs,
+             mode == 0 ? "UC-distinct" : mode == 1 ? "UC-same    " : mode == 2 ? "MC         " : mode == 3 ? "bulk-1d    " : mode == 4 ? "2 half-box " : mode == 5 ? "2 producers" : "4 producers", grid, max_clusters,
              delivered / ms / 1e9, delivered / ms / 1e6 / grid);
       (void)l2_reads;
     }
