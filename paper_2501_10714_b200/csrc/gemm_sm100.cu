@@ -52,6 +52,8 @@ struct KParams {
   int use_peers;           // row-grouped plain stores through `peers`
   fsmoe_dev::PeerRows peers;
   fsmoe_dev::RowRange blocks;  // row-grouped: the blocks this launch covers
+  int dbg;  // measurement only (FSMOE_GEMM_DBG): 1 no epilogue after the TMEM reads,
+            // 2 no TMEM reads either, 4 everything but the TMA stores
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -417,6 +419,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                          p.epi == static_cast<int>(Epi::GeluBwd);
     // this lane's row inside a box: unit k of the row lives at (k ^ (lane & 7))
     auto box_row = [&](uint8_t* box) { return reinterpret_cast<uint4*>(box + lane * 128); };
+    auto store_box = [&](const CUtensorMap* m, const void* box, int x0, int x1, int x2) {
+      if (p.dbg != 4) tma_store_3d(m, box, x0, x1, x2);
+    };
     const int sw = lane & 7;
     int acc = 0;
     uint32_t aph = 0;
@@ -478,6 +483,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // fp32: one 32-column TMEM chunk = one box
         for (int c = CPH * half; c < CPH * half + CPH; ++c) {
           const int col = ti.nt * BN + c * 32;
+          if (p.dbg == 2) break;
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
             tmem_ld_wait();
@@ -487,6 +493,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (c == CPH * half + CPH - 1) release_acc();
           if (col >= p.out_cols) continue;  // warp-uniform
+          if (p.dbg == 1) {
+            if (lane == 0 && (r[0] ^ r[31]) == 0x7fc00001u) r[1] = 0;  // keep the loads
+            continue;
+          }
           uint8_t* box = stg + (c & 1) * 4096;
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
@@ -497,7 +507,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             if (p.accumulate) tma_reduce_add_3d(md, box, col, c1, c2);
-            else tma_store_3d(md, box, col, c1, c2);
+            else store_box(md, box, col, c1, c2);
             bulk_commit();
           }
         }
@@ -507,6 +517,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int c = CPH * half + 2 * pc;
           const int col = ti.nt * BN + c * 32;
           uint32_t r2[32];
+          if (p.dbg == 2) break;
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
             tmem_ld_32x32b_x32(tbase + (c + 1) * 32, r2);
@@ -522,6 +533,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             return *reinterpret_cast<uint32_t*>(&h);
           };
           auto val = [&](int i) { return __uint_as_float(i < 32 ? r[i] : r2[i - 32]); };
+          if (p.dbg == 1) {
+            if (lane == 0 && (r[0] ^ r2[31]) == 0x7fc00001u) r[1] = 0;  // keep the loads
+            continue;
+          }
           if (p.epi == static_cast<int>(Epi::StoreBF16)) {
             uint8_t* box = stg + pc * 4096;
             if (lane == 0) bulk_wait_read<1>();
@@ -534,7 +549,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(md, box, col, c1, c2);
+              store_box(md, box, col, c1, c2);
               bulk_commit();
             }
           } else if (p.epi == static_cast<int>(Epi::GeluFwd)) {
@@ -561,8 +576,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(md, stg, col, c1, c2);
-              tma_store_3d(&em.d2, stg + 4096, col, c1, c2);
+              store_box(md, stg, col, c1, c2);
+              store_box(&em.d2, stg + 4096, col, c1, c2);
               bulk_commit();
             }
           } else {  // GeluBwd: dZ = dH * gelu'(Z), written over the loaded box
@@ -584,7 +599,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(md, box, col, c1, c2);
+              store_box(md, box, col, c1, c2);
               bulk_commit();
             }
           }
@@ -746,6 +761,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.b_mn = pr.b_mn_major ? 1 : 0;
   p.valid = pr.valid_rows;
   p.epi = static_cast<int>(pr.epi);
+  if (const char* env = getenv("FSMOE_GEMM_DBG")) p.dbg = atoi(env);
   p.D = pr.D;
   p.D2 = pr.D2;
   p.Zin = pr.Zin;
