@@ -480,6 +480,11 @@ def gpu_arm(args):
                  "a2a_measured": a2a_meas,
                  "roofline_ms": max(t_gemm, t_a2a), "measured_ms": ms,
                  "frac": max(t_gemm, t_a2a) / ms, "gemm_share_of_step": gms / ms,
+                 # also against the sustained (power-limited, 4 s back
+                 # to back) cuBLAS figure and the 2.25 PFLOP/s spec
+                 "frac_vs_sustained": max(gflops / (peaks.get("bf16_tflops_sustained", 1400.0) * 1e12) * 1e3,
+                                          t_a2a) / ms,
+                 "frac_vs_spec": max(gflops / 2.25e15 * 1e3, t_a2a) / ms,
                  "roofline_tokens_per_s": world * T / (max(t_gemm, t_a2a) * 1e-3)}
 
     cpu = None
