@@ -76,22 +76,32 @@ class ClockSampler:
         self.path = None
 
     def start(self):
+        """Start sampling and return once nvidia-smi is producing lines (its
+        start-up takes a few hundred ms), so short timed regions get samples."""
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        self.n0 = 0
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "20", "-i", str(self.gpu)],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.15)
+            t_end = time.time() + 5.0
+            while time.time() < t_end and self._lines() < 1:
+                time.sleep(0.02)
+            self.n0 = self._lines()   # samples before the timed region are dropped
         except OSError:
             self.proc = None
+
+    def _lines(self):
+        with open(self.path) as f:
+            return sum(1 for _ in f)
 
     def stop(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         if not self.proc:
             return out
-        time.sleep(0.05)
+        time.sleep(0.045)   # at least two more 20 ms samples cover the region's end
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -100,18 +110,19 @@ class ClockSampler:
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
-            for line in f:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 9:
-                    continue
-                try:
-                    sm.append(float(parts[1]))
-                    mx.append(float(parts[2]))
-                except ValueError:
-                    continue
-                for n, v in zip(names, parts[5:9]):
-                    if v.lower().startswith("active"):
-                        reasons.add(n)
+            lines = f.readlines()
+        for line in lines[self.n0:] if len(lines) > self.n0 else lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
         os.unlink(self.path)
         if sm:
             out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons),

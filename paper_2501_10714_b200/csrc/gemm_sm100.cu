@@ -208,6 +208,12 @@ template <int CTAS, int BN_ = BN_MAX>
 struct TileCfg {
   static constexpr int BM = 128 * CTAS;      // tile rows (whole pair)
   static constexpr int BN = BN_;             // tile columns
+  // one tcgen05.mma covers at most 256 columns: a 512-column pair tile issues
+  // two per K step, each over its own 256-row B segment (split over the pair)
+  static constexpr int MMA_N = BN < 256 ? BN : 256;
+  static constexpr int NSEG = BN / MMA_N;
+  static constexpr int SEG_ROWS = MMA_N / CTAS;                // B rows per CTA per segment
+  static constexpr int SEG_BYTES = SEG_ROWS * BK * 2;
   static constexpr int BN_CTA = BN / CTAS;   // B rows staged per CTA
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BN_CTA * BK * 2;
@@ -219,7 +225,10 @@ struct TileCfg {
   static constexpr int NSTAGE = NS_FIT > 6 ? 6 : NS_FIT;
   static constexpr int STG_OFF = NSTAGE * STAGE + 1024;         // after the barrier block
   static constexpr int SMEM = STG_OFF + STG_TOTAL + 1024;
-  static constexpr int TMEM_COLS = 2 * BN;                      // double-buffered accumulator
+  // double-buffered accumulator when two fit in the 512 TMEM columns; the
+  // 512-column tile has one (the MMAs of the next tile wait for the drain)
+  static constexpr int ACC_BUFS = 2 * BN <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = ACC_BUFS * BN;
 };
 
 // Epilogue tensor maps (TMA stores / loads of 32-row x 128-byte SW128 boxes):
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       const int arow = static_cast<int>(rank) * 128;          // this CTA's A rows in the tile
-      const int brow = static_cast<int>(rank) * Cfg::BN_CTA;  // this CTA's B rows in the tile
+      const int brow = static_cast<int>(rank) * Cfg::SEG_ROWS;  // this CTA's B rows per segment
       auto issue = [&](uint8_t* dst, const CUtensorMap* m, int c0, int c1, int c2) {
         if constexpr (CTAS == 2) tma_load_3d_pair(dst, m, mapa_shared(&full_bar[s], 0), c0, c1, c2);
         else tma_load_3d(dst, m, &full_bar[s], c0, c1, c2);
@@ -320,12 +329,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint8_t* sa = smem + s * Cfg::STAGE;
             uint8_t* sb = sa + Cfg::A_BYTES;
             issue(sa, &tmA, kb * BK, p.row0 + ti.mt * Cfg::BM + arow, ti.g);
-            if (!b_mn) {
-              issue(sb, &tmB, kb * BK, ti.nt * BN + brow, w);
-            } else {
 #pragma unroll
-              for (int i = 0; i < Cfg::BN_CTA / 64; ++i)
-                issue(sb + i * 8192, &tmB, ti.nt * BN + brow + i * 64, kb * BK, w);
+            for (int h = 0; h < Cfg::NSEG; ++h) {
+              const int nrow = ti.nt * BN + h * Cfg::MMA_N + brow;
+              uint8_t* sbh = sb + h * Cfg::SEG_BYTES;
+              if (!b_mn) {
+                issue(sbh, &tmB, kb * BK, nrow, w);
+              } else {
+#pragma unroll
+                for (int i = 0; i < Cfg::SEG_ROWS / 64; ++i)
+                  issue(sbh + i * 8192, &tmB, nrow + i * 64, kb * BK, w);
+              }
             }
             if (++s == NS) { s = 0; ph ^= 1; }
           }
@@ -340,8 +354,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int i = 0; i < 2; ++i)
                 issue(sa + i * 8192, &tmA, ti.mt * Cfg::BM + arow + i * 64, p.row0 + kb * BK, b);
 #pragma unroll
-              for (int i = 0; i < Cfg::BN_CTA / 64; ++i)
-                issue(sb + i * 8192, &tmB, ti.nt * BN + brow + i * 64, p.row0 + kb * BK, b);
+              for (int h = 0; h < Cfg::NSEG; ++h)
+#pragma unroll
+                for (int i = 0; i < Cfg::SEG_ROWS / 64; ++i)
+                  issue(sb + h * Cfg::SEG_BYTES + i * 8192, &tmB,
+                        ti.nt * BN + h * Cfg::MMA_N + brow + i * 64, p.row0 + kb * BK, b);
               if (++s == NS) { s = 0; ph ^= 1; }
             }
           }
@@ -351,7 +368,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
     if (leader) {
-      const uint32_t idesc = make_idesc_bf16(Cfg::BM, BN, a_mn, b_mn);
+      const uint32_t idesc = make_idesc_bf16(Cfg::BM, Cfg::MMA_N, a_mn, b_mn);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -373,10 +390,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               uint64_t ad = a_mn ? make_sdesc_sw128(sa + k * 2048, 8192, 1024)
                                  : make_sdesc_sw128(sa + k * 32, 16, 1024);
-              uint64_t bd = b_mn ? make_sdesc_sw128(sb + k * 2048, 8192, 1024)
-                                 : make_sdesc_sw128(sb + k * 32, 16, 1024);
-              if constexpr (CTAS == 2) umma_bf16_pair(dtmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-              else umma_bf16(dtmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+              for (int h = 0; h < Cfg::NSEG; ++h) {
+                const uint32_t sbh = sb + h * Cfg::SEG_BYTES;
+                uint64_t bd = b_mn ? make_sdesc_sw128(sbh + k * 2048, 8192, 1024)
+                                   : make_sdesc_sw128(sbh + k * 32, 16, 1024);
+                const uint32_t dt = dtmem + h * Cfg::MMA_N;
+                if constexpr (CTAS == 2) umma_bf16_pair(dt, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                else umma_bf16(dt, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              }
             }
             if constexpr (CTAS == 2) umma_commit_pair(&empty_bar[s], 0x3);
             else umma_commit(&empty_bar[s]);
@@ -393,7 +415,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         __syncwarp();
-        if (++acc == 2) { acc = 0; aph ^= 1; }
+        if (++acc == Cfg::ACC_BUFS) { acc = 0; aph ^= 1; }
       }
     }
   } else if (warp >= 4) {
@@ -538,7 +560,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             continue;
           }
           if (p.epi == static_cast<int>(Epi::StoreBF16)) {
-            uint8_t* box = stg + pc * 4096;
+            uint8_t* box = stg + (pc & 1) * 4096;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
             uint4* br = box_row(box);
@@ -605,17 +627,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       } else if (p.epi == static_cast<int>(Epi::SwigluFwd)) {
-        // tile cols: [0,128) gate units, [128,256) up units (same 128 units)
+        // every 256 tile columns: [0,128) gate units, [128,256) up units (the
+        // same 128 units). A 256-column tile splits its 128 units over the two
+        // warp halves; a 512-column tile gives each half one 256-column block.
+        constexpr int NSUB = BN >= 256 ? BN / 256 : 1;
+        const int sub = NSUB == 2 ? half : 0;
+        const int c_lo = NSUB == 2 ? 0 : 2 * half;
+        const int c_hi = c_lo + (NSUB == 2 ? 4 : 2);
+        const uint32_t tsub = tbase + sub * 256;
         __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
         __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) + orow * p.ldd2;
-        for (int c = 2 * half; c < 2 * half + 2; ++c) {
+        for (int c = c_lo; c < c_hi; ++c) {
           float g[32];
           if (nkb > 0) {
-            tmem_ld_32x32b_x32(tbase + c * 32, r);
+            tmem_ld_32x32b_x32(tsub + c * 32, r);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) g[i] = __uint_as_float(r[i]);
-            tmem_ld_32x32b_x32(tbase + 128 + c * 32, r);
+            tmem_ld_32x32b_x32(tsub + 128 + c * 32, r);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -623,8 +652,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) g[i] = v[i] = 0.f;
           }
-          const int gcol = ti.nt * BN + c * 32;
-          const int hcol = ti.nt * (BN / 2) + c * 32;
+          const int gcol = ti.nt * BN + sub * 256 + c * 32;
+          const int hcol = ti.nt * (BN / 2) + sub * 128 + c * 32;
           if (row_ok && gcol < p.out_cols) {
             store_bf16x32(Z + gcol, g);
             store_bf16x32(Z + gcol + 128, v);
@@ -670,7 +699,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       if (!released) release_acc();
-      if (++acc == 2) { acc = 0; aph ^= 1; }
+      if (++acc == Cfg::ACC_BUFS) { acc = 0; aph ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();  // outputs written before the kernel retires
     __syncwarp();
@@ -787,15 +816,29 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
                          ((units_cols + BN_MAX - 1) / BN_MAX);
   int ctas = pair_tiles >= num_sms() / 4 ? 2 : 1;
   if (const char* env = getenv("FSMOE_GEMM_CTAS")) ctas = atoi(env) == 1 ? 1 : 2;
-  // Tile width: 256 columns. 128-column tiles (FSMOE_GEMM_BN=128) fill a
-  // ragged last wave better (N = 1024 over 74 SM pairs: 3.46 -> 6.92 waves)
-  // but measured slower on B200 (fwd2 109 -> 130 us: each MMA re-reads A for
-  // half the columns); the layer instead overlaps independent GEMMs on two
-  // streams so one fills the other's tail. SwiGLU needs the 256-column tile.
+  // Tile width. Pairs take 512-column tiles (two MMAs per K step, one
+  // accumulator: 25 % less operand traffic per flop than 256 columns) for the
+  // plain bf16 and fp32 epilogues when that still gives every pair a tile:
+  // measured 2-3 % faster on the configs[1] launches and 8-18 % on the
+  // configs[2] ones (profiles/r01_gemm_bn512.md). The GELU / SwiGLU epilogues
+  // keep 256 columns and double-buffered accumulators (their epilogue is long
+  // enough that the single-accumulator drain shows). 128-column tiles
+  // (FSMOE_GEMM_BN=128) measured slower everywhere. FSMOE_GEMM_BN=128|256|512
+  // forces a width (512: every epilogue but GELU-backward).
   int BN = BN_MAX;
-  if (const char* env = getenv("FSMOE_GEMM_BN"))
-    if (pr.epi != Epi::SwigluFwd && pr.epi != Epi::SwigluBwd) BN = atoi(env) == 128 ? 128 : 256;
-  const int bm = 128 * ctas, bn_cta = BN / ctas;
+  const bool plain_epi = pr.epi == Epi::StoreBF16 || pr.epi == Epi::StoreF32;
+  if (ctas == 2 && plain_epi) {
+    const long long tiles512 = static_cast<long long>(groups) * ((units_rows + 255) / 256) *
+                               ((units_cols + 511) / 512);
+    if (tiles512 >= num_sms() / 2) BN = 512;
+  }
+  if (const char* env = getenv("FSMOE_GEMM_BN")) {
+    const int want = atoi(env);
+    if (want == 128 && pr.epi != Epi::SwigluFwd && pr.epi != Epi::SwigluBwd) BN = 128;
+    else if (want == 256) BN = 256;
+    else if (want == 512 && ctas == 2 && pr.epi != Epi::GeluBwd) BN = 512;
+  }
+  const int bm = 128 * ctas, bn_seg = (BN < 256 ? BN : 256) / ctas;  // B box rows per segment
   if (pr.kind == GemmKind::RowGrouped) {
     if (pr.K % 8 || pr.N % 64 || pr.K <= 0 || pr.N <= 0) return cudaErrorInvalidValue;
     p.m_tiles = (pr.rows + bm - 1) / bm;
@@ -806,7 +849,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     p.out_cols = pr.N;
     if (!make_map3(&ta, pr.A, pr.K, p.rows_total, pr.nblk, BK, 128)) return cudaErrorInvalidValue;
     if (!pr.b_mn_major) {
-      if (!make_map3(&tb, pr.B, pr.K, pr.N, p.n_w, BK, bn_cta)) return cudaErrorInvalidValue;
+      if (!make_map3(&tb, pr.B, pr.K, pr.N, p.n_w, BK, bn_seg)) return cudaErrorInvalidValue;
     } else {
       if (!make_map3(&tb, pr.B, pr.N, pr.K, p.n_w, 64, BK)) return cudaErrorInvalidValue;
     }
@@ -861,9 +904,9 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   const int sms = pr.max_sms > 0 && pr.max_sms < num_sms() ? pr.max_sms : num_sms();
   const int max_units = sms / ctas > 0 ? sms / ctas : 1;
   const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
-  static bool smem_set[2][2] = {{false, false}, {false, false}};
+  static bool smem_set[2][3] = {{false, false, false}, {false, false, false}};
   auto launch = [&](auto kern, int smem) -> cudaError_t {
-    bool& done = smem_set[ctas - 1][BN == 256 ? 1 : 0];
+    bool& done = smem_set[ctas - 1][BN == 128 ? 0 : BN == 256 ? 1 : 2];
     if (!done) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       done = true;
@@ -886,6 +929,8 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   if (ctas == 1)
     e = BN == 256 ? launch(grouped_gemm_kernel<1, 256>, TileCfg<1, 256>::SMEM)
                   : launch(grouped_gemm_kernel<1, 128>, TileCfg<1, 128>::SMEM);
+  else if (BN == 512)
+    e = launch(grouped_gemm_kernel<2, 512>, TileCfg<2, 512>::SMEM);
   else
     e = BN == 256 ? launch(grouped_gemm_kernel<2, 256>, TileCfg<2, 256>::SMEM)
                   : launch(grouped_gemm_kernel<2, 128>, TileCfg<2, 128>::SMEM);

@@ -19,11 +19,12 @@ def _ops():
     return ops
 
 
-@pytest.fixture(params=["1x256", "2x256", "1x128", "2x128"], autouse=True)
+@pytest.fixture(params=["1x256", "2x256", "1x128", "2x128", "2x512"], autouse=True)
 def gemm_ctas(request, monkeypatch):
     """Run every GEMM test on all tile variants: single-CTA (128 rows) and
-    CTA-pair (256 rows, tcgen05 cta_group::2) x 256- and 128-column tiles
-    (SwiGLU epilogues always take 256 columns)."""
+    CTA-pair (256 rows, tcgen05 cta_group::2) x 256- and 128-column tiles,
+    and the pair's 512-column tile (one accumulator, two MMAs per K step;
+    every epilogue but GELU-backward, which keeps 256 columns)."""
     ctas, bn = request.param.split("x")
     monkeypatch.setenv("FSMOE_GEMM_CTAS", ctas)
     monkeypatch.setenv("FSMOE_GEMM_BN", bn)
@@ -155,9 +156,10 @@ def test_gelu_epilogues():
     assert _rel(dZ, g) < 2e-2
 
 
-def test_swiglu_epilogues():
+@pytest.mark.parametrize("H", [256, 640])
+def test_swiglu_epilogues(H):
     ops = _ops()
-    nblk, rows, K, H = 2, 256, 256, 256
+    nblk, rows, K = 2, 256, 256
     X = _rand(nblk, rows, K)
     W1 = _rand(nblk, 2 * H, K, scale=K ** -0.5)  # interleaved [gate128 | up128] blocks
     Z = torch.empty(nblk, rows, 2 * H, device="cuda", dtype=torch.bfloat16)

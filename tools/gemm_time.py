@@ -25,6 +25,8 @@ def t(fn, reps=20):
 
 def main(ffn="simple"):
     E, C, M, H = 16, 1024, 1024, 4096
+    if ffn == "mixtral":  # configs[2] per GPU at N=4: 2 local experts x 4 sources x C 8192
+        ffn, E, C, M, H = "gated3", 2, 32768, 4096, 14336
     N1 = H if ffn == "simple" else 2 * H
     bf = torch.bfloat16
     X = torch.randn(E, C, M, device="cuda").to(bf)
@@ -39,6 +41,7 @@ def main(ffn="simple"):
     gw2 = torch.empty(E, M, H, device="cuda")
     fwd1_epi = "gelu_fwd" if ffn == "simple" else "swiglu_fwd"
     bwd_epi = "gelu_bwd" if ffn == "simple" else "swiglu_bwd"
+    reps = 20 if C * M * H <= 2 ** 32 else 5
     launches = {
         "fwd1": lambda: ops.grouped_gemm("row", X, W1, Z, nblk=E, rows=C, K=M, N=N1, n_w=E,
                                          epi=fwd1_epi, D2=Hh, ldd2=H),
@@ -54,9 +57,10 @@ def main(ffn="simple"):
                                            b_mn_major=True),
     }
     flops = 2.0 * E * C * M * H
+    # (gated3: fwd1 / dgrad2 / wgrad1 do twice this; printed rates use 2*E*C*M*H)
     tot = 0.0
     for name, fn in launches.items():
-        us = t(fn)
+        us = t(fn, reps)
         if name != "fwd1_plain":
             tot += us
         print(f"{name:11s} {us:8.1f} us  {flops / (us * 1e-6) / 1e15:.3f} PFLOP/s")
