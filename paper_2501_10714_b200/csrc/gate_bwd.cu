@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "capi_common.h"
 #include "kernels.h"
@@ -289,6 +290,176 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Paired-column forms of xtg2 / dx_acc2 for fp32-arithmetic tokens (bf16 /
+// fp32 x) with M even: a thread owns columns (j, j+1), so x moves as one
+// 4- or 8-byte load per token and the chunk's G rows are read back from
+// shared memory as float4 broadcasts; the noisy gate's two projections share
+// one pass over x (columns [0, NC) from G1, [NC, 2 NC) from G2). Every output
+// element is accumulated in the same order as in the single-column kernels.
+template <typename XT>
+__device__ __forceinline__ float2 load_pair(const XT* p);
+template <>
+__device__ __forceinline__ float2 load_pair<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+}
+template <>
+__device__ __forceinline__ float2 load_pair<float>(const float* p) {
+  return *reinterpret_cast<const float2*>(p);
+}
+
+template <typename XT, int NCT2>
+__global__ void __launch_bounds__(256)
+    xtg_pair_kernel(int T, int M, int NC, const XT* __restrict__ X, const double* __restrict__ G1,
+                    const double* __restrict__ G2, long long gst, long long gsc,
+                    double* __restrict__ part) {
+  __shared__ __align__(16) float gs[32][NCT2];
+  const int NC2 = G2 ? 2 * NC : NC;
+  const int chunk = blockIdx.y;
+  const int j = (blockIdx.x * 256 + threadIdx.x) * 2;
+  float a0[NCT2], a1[NCT2];
+#pragma unroll
+  for (int c = 0; c < NCT2; ++c) a0[c] = a1[c] = 0.f;
+  const int t_end = min(T, (chunk + 1) * XT_TCH);
+  for (int t0 = chunk * XT_TCH; t0 < t_end; t0 += 32) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * NCT2; i += 256) {
+      const int tt = i / NCT2, c = i % NCT2;
+      const int t = t0 + tt;
+      float v = 0.f;
+      if (t < t_end && c < NC2)
+        v = static_cast<float>(c < NC ? G1[t * gst + c * gsc] : G2[t * gst + (c - NC) * gsc]);
+      gs[tt][c] = v;
+    }
+    __syncthreads();
+    if (j < M) {
+      const int nt = min(32, t_end - t0);
+      // eight tokens' x loads in flight before their FMAs
+      for (int u0 = 0; u0 < nt; u0 += 8) {
+        float2 xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          xv[u] = u0 + u < nt ? load_pair<XT>(X + static_cast<long long>(t0 + u0 + u) * M + j)
+                              : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u0 + u >= nt) break;
+          const float4* g4 = reinterpret_cast<const float4*>(gs[u0 + u]);
+#pragma unroll
+          for (int q = 0; q < NCT2 / 4; ++q) {
+            const float4 g = g4[q];
+            a0[4 * q] += xv[u].x * g.x;
+            a0[4 * q + 1] += xv[u].x * g.y;
+            a0[4 * q + 2] += xv[u].x * g.z;
+            a0[4 * q + 3] += xv[u].x * g.w;
+            a1[4 * q] += xv[u].y * g.x;
+            a1[4 * q + 1] += xv[u].y * g.y;
+            a1[4 * q + 2] += xv[u].y * g.z;
+            a1[4 * q + 3] += xv[u].y * g.w;
+          }
+        }
+      }
+    }
+  }
+  if (j < M) {
+    double* o = part + (static_cast<long long>(chunk) * M + j) * NC2;
+#pragma unroll
+    for (int c = 0; c < NCT2; ++c)
+      if (c < NC2) {
+        o[c] = static_cast<double>(a0[c]);
+        o[NC2 + c] = static_cast<double>(a1[c]);
+      }
+  }
+}
+
+// out1 / out2 (+)= sum_chunk part[chunk][j][c] (fixed order) for the two
+// column groups of xtg_pair_kernel
+__global__ void xtg_reduce_pair_kernel(int nchunks, int M, int NC, int NC2,
+                                       const double* __restrict__ part, double* __restrict__ out1,
+                                       double* __restrict__ out2, long long osj, long long osc,
+                                       int accumulate) {
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(M) * NC2) return;
+  const int j = static_cast<int>(i / NC2), c2 = static_cast<int>(i % NC2);
+  double a = 0.0;
+  for (int k = 0; k < nchunks; ++k) a += part[static_cast<long long>(k) * M * NC2 + i];
+  double* o = c2 < NC ? out1 + j * osj + c2 * osc : out2 + j * osj + (c2 - NC) * osc;
+  *o = accumulate ? *o + a : a;
+}
+
+constexpr int DXP_TOK = 128;  // tokens per block of dx_pair_kernel
+
+template <typename XT, int NCT>
+__global__ void __launch_bounds__(256)
+    dx_pair_kernel(int Tn, int M, int NC, const double* __restrict__ G1, const double* __restrict__ W1,
+                   const double* __restrict__ G2, const double* __restrict__ W2, long long gst,
+                   long long gsc, long long wsj, long long wsc, XT* __restrict__ dx) {
+  __shared__ __align__(16) float gs[2][DXP_TOK][NCT];
+  const int j = (blockIdx.x * 256 + threadIdx.x) * 2;
+  const int t0 = blockIdx.y * DXP_TOK;
+  const int npj = G2 ? 2 : 1;
+  float w1a[NCT], w1b[NCT], w2a[NCT], w2b[NCT];
+#pragma unroll
+  for (int c = 0; c < NCT; ++c) {
+    const bool ok = j < M && c < NC;
+    w1a[c] = ok ? static_cast<float>(W1[j * wsj + c * wsc]) : 0.f;
+    w1b[c] = ok ? static_cast<float>(W1[(j + 1) * wsj + c * wsc]) : 0.f;
+    w2a[c] = ok && G2 ? static_cast<float>(W2[j * wsj + c * wsc]) : 0.f;
+    w2b[c] = ok && G2 ? static_cast<float>(W2[(j + 1) * wsj + c * wsc]) : 0.f;
+  }
+  for (int i = threadIdx.x; i < npj * DXP_TOK * NCT; i += 256) {
+    const int pj = i / (DXP_TOK * NCT), tt = (i / NCT) % DXP_TOK, c = i % NCT;
+    const double* G = pj ? G2 : G1;
+    gs[pj][tt][c] = (t0 + tt < Tn && c < NC) ? static_cast<float>(G[(t0 + tt) * gst + c * gsc]) : 0.f;
+  }
+  __syncthreads();
+  if (j >= M) return;
+  const int nt = min(DXP_TOK, Tn - t0);
+  for (int u0 = 0; u0 < nt; u0 += 8) {
+  // eight tokens' dx loads in flight before their updates
+  float2 dv[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const XT* q = dx + static_cast<long long>(t0 + u0 + u) * M + j;
+    if (u0 + u < nt) {
+      if constexpr (sizeof(XT) == 2) dv[u] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(q));
+      else dv[u] = *reinterpret_cast<const float2*>(q);
+    } else {
+      dv[u] = make_float2(0.f, 0.f);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    if (u0 + u >= nt) break;
+    const int tt = u0 + u;
+    float s0 = 0.f, s1 = 0.f;
+    const float4* g1 = reinterpret_cast<const float4*>(gs[0][tt]);
+#pragma unroll
+    for (int q = 0; q < NCT / 4; ++q) {
+      const float4 g = g1[q];
+      s0 += g.x * w1a[4 * q]; s0 += g.y * w1a[4 * q + 1]; s0 += g.z * w1a[4 * q + 2]; s0 += g.w * w1a[4 * q + 3];
+      s1 += g.x * w1b[4 * q]; s1 += g.y * w1b[4 * q + 1]; s1 += g.z * w1b[4 * q + 2]; s1 += g.w * w1b[4 * q + 3];
+    }
+    if (G2) {
+      const float4* g2 = reinterpret_cast<const float4*>(gs[1][tt]);
+#pragma unroll
+      for (int q = 0; q < NCT / 4; ++q) {
+        const float4 g = g2[q];
+        s0 += g.x * w2a[4 * q]; s0 += g.y * w2a[4 * q + 1]; s0 += g.z * w2a[4 * q + 2]; s0 += g.w * w2a[4 * q + 3];
+        s1 += g.x * w2b[4 * q]; s1 += g.y * w2b[4 * q + 1]; s1 += g.z * w2b[4 * q + 2]; s1 += g.w * w2b[4 * q + 3];
+      }
+    }
+    XT* p = dx + static_cast<long long>(t0 + tt) * M + j;
+    const float2 d = dv[u];
+    if constexpr (sizeof(XT) == 2) {
+      *reinterpret_cast<__nv_bfloat162*>(p) = __halves2bfloat162(__float2bfloat16(d.x + s0), __float2bfloat16(d.y + s1));
+    } else {
+      *reinterpret_cast<float2*>(p) = make_float2(static_cast<float>(static_cast<double>(d.x) + static_cast<double>(s0)),
+                                                  static_cast<float>(static_cast<double>(d.y) + static_cast<double>(s1)));
+    }
+  }
+  }
+}
+
 struct Ws {
   char* p;
   double* take(size_t n) {
@@ -308,6 +479,34 @@ void xtg2_launch(int xdt, int T, int M, int NC, const void* X, const double* G, 
     default: xtg2_kernel<2, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
   }
   ::fsmoe::count_launch();
+}
+
+// x^T [G1 | G2] in one pass (fp32-arithmetic tokens, M even, 2 NC <= 32);
+// false when the shape needs the general kernels
+bool xtg_pair(int xdt, int T, int M, int NC, const void* X, const double* G1, const double* G2,
+              long long gst, long long gsc, double* out1, double* out2, long long osj, long long osc,
+              int accumulate, double* part, cudaStream_t st) {
+  const int NC2 = G2 ? 2 * NC : NC;
+  if (xdt == FSMOE_F64 || M % 2 || NC2 > 32) return false;
+  const int nchunks = (T + XT_TCH - 1) / XT_TCH;
+  dim3 grid((M / 2 + 255) / 256, nchunks);
+  auto go = [&](auto nct) {
+    constexpr int N = decltype(nct)::value;
+    if (xdt == FSMOE_F32)
+      xtg_pair_kernel<float, N><<<grid, 256, 0, st>>>(T, M, NC, static_cast<const float*>(X), G1, G2, gst, gsc, part);
+    else
+      xtg_pair_kernel<__nv_bfloat16, N><<<grid, 256, 0, st>>>(T, M, NC, static_cast<const __nv_bfloat16*>(X), G1,
+                                                                G2, gst, gsc, part);
+    ::fsmoe::count_launch();
+  };
+  if (NC2 <= 8) go(std::integral_constant<int, 8>{});
+  else if (NC2 <= 16) go(std::integral_constant<int, 16>{});
+  else go(std::integral_constant<int, 32>{});
+  const long long n = static_cast<long long>(M) * NC2;
+  xtg_reduce_pair_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(nchunks, M, NC, NC2, part, out1,
+                                                                            G2 ? out2 : out1, osj, osc, accumulate);
+  ::fsmoe::count_launch();
+  return true;
 }
 
 void xtg(int xdt, int T, int M, int NC, const void* X, const double* G, long long gst,
@@ -354,6 +553,22 @@ bool dx_acc_pair(int xdt, int T, int M, int NC, const double* G1, const double* 
                  const double* G2, const double* W2, long long gst, long long gsc, long long wsj,
                  long long wsc, void* dx, cudaStream_t st) {
   if (NC > 64) return false;
+  if (xdt != FSMOE_F64 && M % 2 == 0 && NC <= 16) {
+    dim3 grid((M / 2 + 255) / 256, (T + DXP_TOK - 1) / DXP_TOK);
+    auto go = [&](auto nct) {
+      constexpr int N = decltype(nct)::value;
+      if (xdt == FSMOE_F32)
+        dx_pair_kernel<float, N><<<grid, 256, 0, st>>>(T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc,
+                                                       static_cast<float*>(dx));
+      else
+        dx_pair_kernel<__nv_bfloat16, N><<<grid, 256, 0, st>>>(T, M, NC, G1, W1, G2, W2, gst, gsc, wsj,
+                                                               wsc, static_cast<__nv_bfloat16*>(dx));
+      ::fsmoe::count_launch();
+    };
+    if (NC <= 8) go(std::integral_constant<int, 8>{});
+    else go(std::integral_constant<int, 16>{});
+    return true;
+  }
   if (NC <= 8) dx_acc2_launch<8>(xdt, T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, dx, st);
   else if (NC <= 16) dx_acc2_launch<16>(xdt, T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, dx, st);
   else if (NC <= 32) dx_acc2_launch<32>(xdt, T, M, NC, G1, W1, G2, W2, gst, gsc, wsj, wsc, dx, st);
@@ -380,7 +595,8 @@ size_t gate_bwd_workspace_bytes(const fsmoe_gate_desc& d) {
   size_t nc = E > P ? E : P;
   size_t wide = M > P ? M : P;
   auto r = [](size_t n) { return (n * 8 + 255) & ~size_t(255); };
-  return r(T * E) * 2 + r(T * P) * 2 + r(nch * wide * (nc > 0 ? nc : 1)) + r(P * E) + r(E) * 2 + 1024;
+  // partials hold two column groups (xtg_pair: the noisy gate's dS | dZ)
+  return r(T * E) * 2 + r(T * P) * 2 + r(nch * wide * 2 * (nc > 0 ? nc : 1)) + r(P * E) + r(E) * 2 + 1024;
 }
 
 int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
@@ -400,15 +616,17 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
   const int nch = (T + XT_TCH - 1) / XT_TCH;
   const int P = d.proj_rows > 0 ? d.proj_rows : 0;
   const int nc = E > P ? E : P;
-  double* part = w.take(static_cast<size_t>(nch) * (M > P ? M : P) * (nc > 0 ? nc : 1));
+  double* part = w.take(static_cast<size_t>(nch) * (M > P ? M : P) * 2 * (nc > 0 ? nc : 1));
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
       dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dZ = w.take(static_cast<size_t>(T) * E);
       long long n = static_cast<long long>(T) * E;
       noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ); ::fsmoe::count_launch();
-      xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
-      xtg(d.x_dtype, T, M, E, x, dZ, E, 1, dWn, E, 1, 1, part, st);
+      if (!xtg_pair(d.x_dtype, T, M, E, x, dS, dZ, E, 1, dWs, dWn, E, 1, 1, part, st)) {
+        xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
+        xtg(d.x_dtype, T, M, E, x, dZ, E, 1, dWn, E, 1, 1, part, st);
+      }
       if (!dx_acc_pair(d.x_dtype, T, M, E, dS, w_score, dZ, w_noise, E, 1, E, 1, dx, st)) {
         dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
         dx_acc(d.x_dtype, T, M, E, dZ, E, 1, w_noise, E, 1, dx, st);
@@ -417,7 +635,8 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
     }
     case FSMOE_GATE_SIGMOID_TOPK: {
       dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(1, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
-      xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
+      if (!xtg_pair(d.x_dtype, T, M, E, x, dS, nullptr, E, 1, dWs, nullptr, E, 1, 1, part, st))
+        xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
       dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
       break;
     }
