@@ -265,7 +265,7 @@ def gemm_roofline(layer, peaks, reps=5):
     return {
         "bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
         "frac": round(achieved / peak, 4), "traffic": None,
-        "kernel": "grouped_gemm_kernel (tcgen05, 6 launches/step: fwd1 fwd2 wgrad2 dgrad2 wgrad1 dgrad1)",
+        "kernel": "grouped_gemm_kernel (tcgen05 cta_group::2; 6 launches/step: fwd1 (256x256 tiles, GELU) fwd2 wgrad2 (256x512) dgrad2 (256x256, GELU bwd) wgrad1 dgrad1 (256x512))",
         "flops_per_step": flops, "gemm_ms_per_step": round(ms, 4),
         "per_launch_ms": {k: round(v[1], 4) for k, v in per.items()},
         "peak_kind": "bf16_tflops (burst) of MEASURED_PEAKS.json",
