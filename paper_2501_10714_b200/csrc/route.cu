@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256)
 // destination (local or a peer's buffer over NVLink). One instruction moves a
 // whole row, so the LSU / register path that limits the warp-per-row copy
 // (long-scoreboard + lg_throttle stalls, ncu) drops out.
-constexpr int BK_ROWS = 32;  // rows per block (one warp)
+constexpr int BK_ROWS = 32;  // rows per group (one per lane)
 
 __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
@@ -252,30 +252,38 @@ __global__ void __launch_bounds__(32)
   extern __shared__ __align__(128) uint8_t sm[];  // [BK_ROWS][row_bytes] + one zero row
   __shared__ __align__(8) uint64_t bar;
   const int lane = threadIdx.x;
-  const long long s = blockIdx.x * static_cast<long long>(BK_ROWS) + lane;
   uint8_t* zero = sm + BK_ROWS * row_bytes;
   for (int i = lane * 16; i < row_bytes; i += 32 * 16) *reinterpret_cast<uint4*>(zero + i) = make_uint4(0, 0, 0, 0);
   if (lane == 0) {
     fsmoe_dev::mbar_init(&bar, 32);
     fsmoe_dev::fence_barrier_init();
   }
-  __syncwarp();
-  int p = -1;
-  const bool valid = s < n_slots && in_range(rr, s);
-  if (valid) p = pick_of_slot[s];
-  uint8_t* mine = sm + lane * row_bytes;
-  if (p >= 0) {
-    fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
-    fsmoe_dev::bulk_load(mine, x + static_cast<long long>(ptok[p]) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
-  } else {
-    fsmoe_dev::mbar_arrive(&bar);
-  }
   fsmoe_dev::fence_proxy_async_smem();  // the zero row (generic writes) -> async proxy
-  fsmoe_dev::mbar_wait(&bar, 0);
-  if (valid) {
-    char* dst = peer_row(buf, slot_row(s, E, C, chunks), row_bytes);
-    bulk_store(dst, p >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
-    fsmoe_dev::bulk_commit();
+  __syncwarp();
+  uint8_t* mine = sm + (lane % BK_ROWS) * row_bytes;
+  const long long ngroups = (n_slots + BK_ROWS - 1) / BK_ROWS;
+  uint32_t phase = 0;
+  // persistent: a block walks groups of BK_ROWS slots (lanes >= BK_ROWS idle)
+  for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const long long s = g * BK_ROWS + lane;
+    int p = -1;
+    const bool valid = lane < BK_ROWS && s < n_slots && in_range(rr, s);
+    if (valid) p = pick_of_slot[s];
+    if (p >= 0) {
+      fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
+      fsmoe_dev::bulk_load(mine, x + static_cast<long long>(ptok[p]) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
+    } else {
+      fsmoe_dev::mbar_arrive(&bar);
+    }
+    fsmoe_dev::mbar_wait(&bar, phase);
+    phase ^= 1u;
+    if (valid) {
+      char* dst = peer_row(buf, slot_row(s, E, C, chunks), row_bytes);
+      bulk_store(dst, p >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
+      fsmoe_dev::bulk_commit();
+    }
+    fsmoe_dev::bulk_wait_read<0>();  // the row buffer is free for the next group
+    __syncwarp();
   }
   fsmoe_dev::bulk_wait<0>();  // shared memory must outlive the stores
 }
@@ -290,30 +298,57 @@ __global__ void __launch_bounds__(32)
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ __align__(8) uint64_t bar;
   const int lane = threadIdx.x;
-  const long long i = blockIdx.x * static_cast<long long>(BK_ROWS) + lane;
   uint8_t* zero = sm + BK_ROWS * row_bytes;
   for (int b = lane * 16; b < row_bytes; b += 32 * 16) *reinterpret_cast<uint4*>(zero + b) = make_uint4(0, 0, 0, 0);
   if (lane == 0) {
     fsmoe_dev::mbar_init(&bar, 32);
     fsmoe_dev::fence_barrier_init();
   }
-  __syncwarp();
-  const bool valid = i < n_rows;
-  const int s = valid ? idx[i] : -1;
-  uint8_t* mine = sm + lane * row_bytes;
-  if (s >= 0) {
-    fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
-    fsmoe_dev::bulk_load(mine, src + static_cast<long long>(s) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
-  } else {
-    fsmoe_dev::mbar_arrive(&bar);
-  }
   fsmoe_dev::fence_proxy_async_smem();
-  fsmoe_dev::mbar_wait(&bar, 0);
-  if (valid) {
-    bulk_store(peer_row(dst, i, row_bytes), s >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
-    fsmoe_dev::bulk_commit();
+  __syncwarp();
+  uint8_t* mine = sm + (lane % BK_ROWS) * row_bytes;
+  const long long ngroups = (n_rows + BK_ROWS - 1) / BK_ROWS;
+  uint32_t phase = 0;
+  for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const long long i = g * BK_ROWS + lane;
+    const bool valid = lane < BK_ROWS && i < n_rows;
+    const int s = valid ? idx[i] : -1;
+    if (s >= 0) {
+      fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
+      fsmoe_dev::bulk_load(mine, src + static_cast<long long>(s) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
+    } else {
+      fsmoe_dev::mbar_arrive(&bar);
+    }
+    fsmoe_dev::mbar_wait(&bar, phase);
+    phase ^= 1u;
+    if (valid) {
+      bulk_store(peer_row(dst, i, row_bytes), s >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
+      fsmoe_dev::bulk_commit();
+    }
+    fsmoe_dev::bulk_wait_read<0>();
+    __syncwarp();
   }
   fsmoe_dev::bulk_wait<0>();
+}
+
+// persistent grid for the bulk row movers: every resident block slot, at
+// most one block per group
+template <typename K>
+int bulk_grid(K kern, int smem, long long ngroups) {
+  static int cached_smem = -1, per_sm = 1;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (smem != cached_smem) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    cached_smem = smem;
+  }
+  const long long slots = static_cast<long long>(per_sm) * sms;
+  return static_cast<int>(ngroups < slots ? ngroups : slots);
 }
 
 // ---------------------------------------------------------------- combine --
@@ -677,8 +712,8 @@ int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, co
     cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
     attr = true;
   }
-  gather_bulk_kernel<<<static_cast<int>((n_rows + BK_ROWS - 1) / BK_ROWS), 32,
-                       static_cast<int>((BK_ROWS + 1) * row_bytes), st>>>(
+  const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
+  gather_bulk_kernel<<<bulk_grid(gather_bulk_kernel, smem, (n_rows + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
       n_rows, static_cast<int>(row_bytes), idx, static_cast<const uint8_t*>(src), dst);
   ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_gather_rows");
@@ -698,7 +733,7 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
       cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
       attr = true;
     }
-    dispatch_bulk_kernel<<<static_cast<int>((n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
+    dispatch_bulk_kernel<<<bulk_grid(dispatch_bulk_kernel, smem, (n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
         n_slots, static_cast<int>(row_bytes), E, C, chunks, pick_of_slot, ptok,
         static_cast<const uint8_t*>(x), buf, rr);
     ::fsmoe::count_launch();
