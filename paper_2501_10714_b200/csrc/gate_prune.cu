@@ -60,11 +60,24 @@ __global__ void w_prep_kernel(int M, int Ea, const double* __restrict__ Wa, int 
   const int NC = Ea + Eb;
   const int c = blockIdx.x;
   double ss = 0.0;
-  for (int j = threadIdx.x; j < M; j += blockDim.x) {
-    double v = c < Ea ? Wa[static_cast<long long>(j) * Ea + c] : Wb[static_cast<long long>(j) * Eb + (c - Ea)];
-    W32[static_cast<long long>(j) * NC + c] = static_cast<float>(v);
-    WT[static_cast<long long>(c) * M + j] = v;
-    ss = __fma_rn(v, v, ss);
+  // eight rows' loads in flight per thread before their uses (the column is
+  // strided in W: each load is its own line, so latency dominates)
+  for (int j0 = threadIdx.x; j0 < M; j0 += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u * blockDim.x;
+      v[u] = j >= M ? 0.0
+                    : c < Ea ? Wa[static_cast<long long>(j) * Ea + c] : Wb[static_cast<long long>(j) * Eb + (c - Ea)];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u * blockDim.x;
+      if (j >= M) break;
+      W32[static_cast<long long>(j) * NC + c] = static_cast<float>(v[u]);
+      WT[static_cast<long long>(c) * M + j] = v[u];
+      ss = __fma_rn(v[u], v[u], ss);
+    }
   }
   __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
