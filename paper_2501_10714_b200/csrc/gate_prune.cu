@@ -29,11 +29,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <cstdlib>
 #include <cstdio>
 #include <algorithm>
 #include <vector>
 
+#include "host_once.h"
 #include "capi_common.h"
 #include "kernels.h"
 #include "route_common.cuh"
@@ -437,10 +439,9 @@ void launch_exact(const void* x, int T, int M, int E, const PruneWsView& w, cuda
                       (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   if (staged) {
     constexpr int SMEM = 2 * (EX_TOK * Elem<DT>::ROW + NPROJ * Elem<DT>::JC * 8);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned> attr{0};
+    if (first_on_device(attr)) {
       cudaFuncSetAttribute(exact_staged_kernel<DT, NPROJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-      attr = true;
     }
     dim3 g((T + EX_TOK - 1) / EX_TOK, E);
     exact_staged_kernel<DT, NPROJ><<<g, EX_TOK * NPROJ, SMEM, st>>>(x, T, M, E, w.WT, w.lists, w.counts,
@@ -1171,20 +1172,18 @@ void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const floa
   const double u = 0x1.0p-24;
   const double gam = M * u / (1.0 - M * u);
   constexpr int SMEM = ScreenSmem<NCP, E_MAX>::BYTES;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(screen_kernel<KIND, NCP, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
   }
   const auto* xb = static_cast<const __nv_bfloat16*>(x);
   screen_kernel<KIND, NCP, E_MAX><<<(T + SC_TOK - 1) / SC_TOK, 512 + SC_MT_WARPS * 32, SMEM, st>>>(
       xb, T, M, E, k, W32, NC, wn, cB, gam, d.seed, noise_ws, scores_out, spread_out, mask);
   ::fsmoe::count_launch();
   constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
-  static bool xattr = false;
-  if (!xattr) {
+  static std::atomic<unsigned> xattr{0};
+  if (first_on_device(xattr)) {
     cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM);
-    xattr = true;
   }
   exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, XSMEM, st>>>(
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,

@@ -22,6 +22,7 @@
 #include <mutex>
 
 #include "gemm.h"
+#include "host_once.h"
 #include "sm100.cuh"
 
 namespace fsmoe {
@@ -904,13 +905,10 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   const int sms = pr.max_sms > 0 && pr.max_sms < num_sms() ? pr.max_sms : num_sms();
   const int max_units = sms / ctas > 0 ? sms / ctas : 1;
   const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
-  static bool smem_set[2][3] = {{false, false, false}, {false, false, false}};
+  static std::atomic<unsigned> smem_set[2][3];
   auto launch = [&](auto kern, int smem) -> cudaError_t {
-    bool& done = smem_set[ctas - 1][BN == 128 ? 0 : BN == 256 ? 1 : 2];
-    if (!done) {
+    if (first_on_device(smem_set[ctas - 1][BN == 128 ? 0 : BN == 256 ? 1 : 2]))
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      done = true;
-    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(units * ctas);
     cfg.blockDim = dim3(NUM_THREADS);

@@ -18,9 +18,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <type_traits>
 #include <cstdlib>
 
+#include "host_once.h"
 #include "capi_common.h"
 #include "kernels.h"
 #include "route_common.cuh"
@@ -707,10 +709,9 @@ int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, co
   if (n_rows <= 0) return FSMOE_OK;
   if (row_bytes % 16 != 0 || row_bytes > 4096)
     return config_error("gather_rows: row bytes must be a multiple of 16 and at most 4096");
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
-    attr = true;
   }
   const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
   gather_bulk_kernel<<<bulk_grid(gather_bulk_kernel, smem, (n_rows + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
@@ -728,10 +729,9 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
   const int grid = static_cast<int>((n_slots + 7) / 8);
   if (row_bytes % 16 == 0 && row_bytes <= 4096 && !getenv("FSMOE_ROUTE_NOBULK")) {
     const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned> attr{0};
+    if (first_on_device(attr)) {
       cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
-      attr = true;
     }
     dispatch_bulk_kernel<<<bulk_grid(dispatch_bulk_kernel, smem, (n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
         n_slots, static_cast<int>(row_bytes), E, C, chunks, pick_of_slot, ptok,

@@ -237,3 +237,28 @@ def test_row_window_chunks(kind):
         for b in range(nblk):
             ref[b % 2] += A[b].double().T @ G[b].double()
         assert _rel(W, ref) < 5e-3
+
+
+def test_two_devices_one_process(gemm_ctas):
+    """Kernel attributes (dynamic shared memory) are per device: a process
+    that drives two GPUs must get correct GEMMs and row moves on both."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    ops = _ops()
+    E, C, K, N = 4, 256, 256, 512
+    for dev in (0, 1):
+        with torch.cuda.device(dev):
+            X = (torch.randn(E, C, K, device="cuda")).to(torch.bfloat16)
+            W = (torch.randn(E, N, K, device="cuda") * K ** -0.5).to(torch.bfloat16)
+            Z = torch.empty(E, C, N, device="cuda", dtype=torch.bfloat16)
+            ops.grouped_gemm("row", X, W, Z, nblk=E, rows=C, K=K, N=N, n_w=E)
+            idx = torch.randperm(E * C, device="cuda").to(torch.int32)
+            idx[::7] = -1
+            src = X.view(E * C, K)
+            out = ops.gather_rows(src, idx)
+            torch.cuda.synchronize()
+            ref = torch.stack([X[b].float() @ W[b].float().T for b in range(E)])
+            assert _rel(Z, ref) < 2e-2
+            keep = idx >= 0
+            assert torch.equal(out[keep], src[idx[keep].long()])
+            assert int(out[~keep].abs().sum()) == 0
