@@ -47,8 +47,15 @@ WORKLOADS = {
                     d_model=4096, d_ffn=14336, experts=8, top_k=2, gate="noisy_topk (GShard top-2)",
                     ffn="gated3 (SwiGLU)", capacity_factor=1.0, dtype="bf16 / fp32 accumulate",
                     l2="inputs and activations larger than L2 (126 MB): no flush needed"),
+    # GPT-2-XL-shape layer for the other gates (--gate), 4096
+    # tokens per GPU (B 4 x L 1024), 8 experts top-2, C = 1024
+    "gpt2xl": dict(workload="GPT-2-XL-shape MoE layer (SURVEY C5)", tokens_per_gpu=4096, d_model=1600,
+                   d_ffn=6400, experts=8, top_k=2, gate="noisy_topk", ffn="simple (GELU)",
+                   capacity_factor=1.0, dtype="bf16 / fp32 accumulate",
+                   l2="weights + activations ~0.3 GB per step (> L2): no flush needed"),
 }
 WORKLOAD = WORKLOADS["gpt2m"]
+GATES = ("noisy_topk", "sigmoid_topk", "cosine_topk", "expert_choice")
 NVLINK_GBS = 900.0  # nominal per direction per GPU (measured peer copy ~770)
 
 
@@ -315,8 +322,12 @@ def gpu_arm(args):
     peaks, peak_kind = load_peaks()
     T, M, H, E = (WORKLOAD["tokens_per_gpu"], WORKLOAD["d_model"], WORKLOAD["d_ffn"],
                   WORKLOAD["experts"])
-    cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=WORKLOAD["top_k"],
-                    gate="noisy_topk", ffn=WORKLOAD["ffn"].split()[0], capacity_factor=1.0,
+    gate = args.gate or WORKLOAD["gate"].split()[0]
+    # expert choice: every expert takes C = k f T / E tokens (workload.cpp:156-171,
+    # the layer derives C from k); cosine: a 64-row projection (the reference
+    # leaves the dimension open)
+    cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=WORKLOAD["top_k"], gate=gate, ffn=WORKLOAD["ffn"].split()[0], capacity_factor=1.0,
+                    proj_dim=64 if gate == "cosine_topk" else 0,
                     precision="bf16", seed=7, r_fwd=args.r_fwd, r_bwd=args.r_bwd)
     ep = EpGroup(world, rank, local, max_ctas=args.nccl_ctas) if world > 1 else None
     layer = MoELayer(cfg, ep, init_seed=1)
@@ -530,7 +541,7 @@ def gpu_arm(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random tokens, random-init experts)",
             "config": dict(WORKLOAD, parallelism=f"ep{world}", r_fwd=args.r_fwd, r_bwd=args.r_bwd,
-                           capacity=C),
+                           capacity=C, **({"gate": gate} if args.gate else {})),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches,
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu,
         }
@@ -558,7 +569,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", default="", help="write per-rank measured timelines to PATH.rankN.json")
     ap.add_argument("--config", default="gpt2m", choices=sorted(WORKLOADS),
-                    help="gpt2m = BASELINE configs[1] (the headline); mixtral = configs[2]")
+                    help="gpt2m = BASELINE configs[1] (the headline); mixtral = configs[2]; "
+                         "gpt2xl = SURVEY C5 (use with --gate)")
+    ap.add_argument("--gate", default=None, choices=GATES,
+                    help="gate kind (default: the workload's, noisy_topk)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     global WORKLOAD
