@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "capi_common.h"
 #include "kernels.h"
@@ -34,7 +35,7 @@ namespace {
 using namespace fsmoe_dev;
 
 constexpr int RD_THREADS = 128;  // tokens per block (one per thread)
-constexpr int RD_CG = 8;         // output columns per thread
+constexpr int RD_CG = 8;         // output columns per thread (fewer when that leaves SMs idle)
 
 struct RowdotJob {
   const double* W;  // W(j, c) = W[j*wsj + c*wsc]
@@ -54,27 +55,27 @@ template <> struct Stage<0> { using T = double; static constexpr int JC = 32; };
 // noisy gate's two projections (x W_g, x W_noise) are one launch. The token
 // chunk is staged transposed in smem (conflict-free reads), the weight chunk
 // as broadcast rows.
-template <int DT>
+template <int DT, int CG>
 __global__ void __launch_bounds__(RD_THREADS)
     rowdot_kernel(const void* __restrict__ x, int T, int M, RowdotJob ja, RowdotJob jb,
                   int groups_a) {
   using ST = typename Stage<DT>::T;
   constexpr int JC = Stage<DT>::JC;
   __shared__ ST xs[JC][RD_THREADS + 1];  // +1: conflict-free transposed stores
-  __shared__ __align__(16) double ws[JC][RD_CG];
+  __shared__ __align__(16) double ws[JC][CG];
   const bool second = static_cast<int>(blockIdx.y) >= groups_a;
   const RowdotJob& J = second ? jb : ja;
-  const int c0 = (second ? blockIdx.y - groups_a : blockIdx.y) * RD_CG;
+  const int c0 = (second ? blockIdx.y - groups_a : blockIdx.y) * CG;
   const int t0 = blockIdx.x * RD_THREADS;
   const int t = t0 + threadIdx.x;
-  double acc[RD_CG];
+  double acc[CG];
 #pragma unroll
-  for (int c = 0; c < RD_CG; ++c) acc[c] = 0.0;
+  for (int c = 0; c < CG; ++c) acc[c] = 0.0;
   for (int j0 = 0; j0 < M; j0 += JC) {
     const int jn = (M - j0) < JC ? (M - j0) : JC;
     __syncthreads();
-    for (int i = threadIdx.x; i < JC * RD_CG; i += RD_THREADS) {
-      int jj = i / RD_CG, cc = i % RD_CG;
+    for (int i = threadIdx.x; i < JC * CG; i += RD_THREADS) {
+      int jj = i / CG, cc = i % CG;
       int c = c0 + cc;
       ws[jj][cc] = (jj < jn && c < J.NC) ? J.W[(j0 + jj) * J.wsj + c * J.wsc] : 0.0;
     }
@@ -89,19 +90,23 @@ __global__ void __launch_bounds__(RD_THREADS)
 #pragma unroll 4
       for (int jj = 0; jj < jn; ++jj) {
         const double xv = static_cast<double>(xs[jj][threadIdx.x]);
-        const double2* w2 = reinterpret_cast<const double2*>(ws[jj]);
+        if constexpr (CG >= 2) {
+          const double2* w2 = reinterpret_cast<const double2*>(ws[jj]);
 #pragma unroll
-        for (int c = 0; c < RD_CG / 2; ++c) {
-          const double2 w = w2[c];
-          acc[2 * c] = mul_add_rn(acc[2 * c], xv, w.x);
-          acc[2 * c + 1] = mul_add_rn(acc[2 * c + 1], xv, w.y);
+          for (int c = 0; c < CG / 2; ++c) {
+            const double2 w = w2[c];
+            acc[2 * c] = mul_add_rn(acc[2 * c], xv, w.x);
+            acc[2 * c + 1] = mul_add_rn(acc[2 * c + 1], xv, w.y);
+          }
+        } else {
+          acc[0] = mul_add_rn(acc[0], xv, ws[jj][0]);
         }
       }
     }
   }
   if (t < T) {
 #pragma unroll
-    for (int c = 0; c < RD_CG; ++c)
+    for (int c = 0; c < CG; ++c)
       if (c0 + c < J.NC) J.out[t * J.ost + (c0 + c) * J.osc] = acc[c];
   }
 }
@@ -418,14 +423,33 @@ int gate_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
     w += (bytes + 255) & ~size_t(255);
     return reinterpret_cast<double*>(p);
   };
+  // columns per thread: 8 independent fp64 chains per thread, unless that
+  // leaves the grid too small to fill the GPU (few tokens or columns: the
+  // expert-choice logits, E = 8) -- then fewer chains and more threads
   auto rowdot2 = [&](RowdotJob a, RowdotJob b) {
-    const int ga = (a.NC + RD_CG - 1) / RD_CG, gb = b.W ? (b.NC + RD_CG - 1) / RD_CG : 0;
-    dim3 grid((T + RD_THREADS - 1) / RD_THREADS, ga + gb);
-    switch (d.x_dtype) {
-      case FSMOE_F64: rowdot_kernel<0><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
-      case FSMOE_F32: rowdot_kernel<1><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
-      default: rowdot_kernel<2><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
-    }
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long tb = (T + RD_THREADS - 1) / RD_THREADS;
+    auto blocks = [&](int cg) {
+      return tb * ((a.NC + cg - 1) / cg + (b.W ? (b.NC + cg - 1) / cg : 0));
+    };
+    int cg = RD_CG;
+    while (cg > 1 && blocks(cg) < 2LL * sms) cg /= 2;
+    auto go = [&](auto cgc) {
+      constexpr int CG = decltype(cgc)::value;
+      const int ga = (a.NC + CG - 1) / CG, gb = b.W ? (b.NC + CG - 1) / CG : 0;
+      dim3 grid(static_cast<unsigned>(tb), ga + gb);
+      switch (d.x_dtype) {
+        case FSMOE_F64: rowdot_kernel<0, CG><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
+        case FSMOE_F32: rowdot_kernel<1, CG><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
+        default: rowdot_kernel<2, CG><<<grid, RD_THREADS, 0, st>>>(x, T, M, a, b, ga); break;
+      }
+    };
+    if (cg == 8) go(std::integral_constant<int, 8>{});
+    else if (cg == 4) go(std::integral_constant<int, 4>{});
+    else if (cg == 2) go(std::integral_constant<int, 2>{});
+    else go(std::integral_constant<int, 1>{});
     ::fsmoe::count_launch();
   };
   auto rowdot = [&](const double* W, long long wsj, long long wsc, int NC, double* out,
