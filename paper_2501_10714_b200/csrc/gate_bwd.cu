@@ -71,31 +71,30 @@ __global__ void noisy_dz_kernel(long long n, const double* __restrict__ dS,
   if (i < n) dZ[i] = dS[i] * noise[i] / (1.0 + exp(-spread[i]));
 }
 
-// cosine, per token: dq[t] = sum_e dS[t][e] (w_e/(|q||w_e|) - s_e q/|q|^2);
-// qn[t] = q/|q|.
+// cosine: dq[t][p] = sum_e dS[t][e] (w_pe/(|q||w_e|) - s_e q_p/|q|^2);
+// qn[t] = q/|q|. One thread per (token, p) -- the same operations in the same
+// order as a per-token loop, with T x P threads to spread the fp64 divisions.
 __global__ void cosine_dq_kernel(int T, int E, int P, const double* __restrict__ q,
                                  const double* __restrict__ w, const double* __restrict__ enorm,
                                  const double* __restrict__ s, const double* __restrict__ dS,
                                  double* __restrict__ dq, double* __restrict__ qn) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(T) * P) return;
+  const int t = static_cast<int>(i / P), p = static_cast<int>(i % P);
   const double* qt = q + static_cast<long long>(t) * P;
   double pn = 0.0;
-  for (int p = 0; p < P; ++p) pn += qt[p] * qt[p];
+  for (int pp = 0; pp < P; ++pp) pn += qt[pp] * qt[pp];
   const double qnorm = sqrt(pn);
-  double* d = dq + static_cast<long long>(t) * P;
-  for (int p = 0; p < P; ++p) {
-    d[p] = 0.0;
-    qn[static_cast<long long>(t) * P + p] = qt[p] / qnorm;
-  }
+  qn[i] = qt[p] / qnorm;
+  double d = 0.0;
   for (int e = 0; e < E; ++e) {
-    double g = dS[static_cast<long long>(t) * E + e];
+    const double g = dS[static_cast<long long>(t) * E + e];
     if (g == 0.0) continue;
-    double wn = sqrt(enorm[e]);
-    double se = s[static_cast<long long>(t) * E + e];
-    for (int p = 0; p < P; ++p)
-      d[p] += g * (w[static_cast<long long>(p) * E + e] / (qnorm * wn) - se * qt[p] / pn);
+    const double wn = sqrt(enorm[e]);
+    const double se = s[static_cast<long long>(t) * E + e];
+    d += g * (w[static_cast<long long>(p) * E + e] / (qnorm * wn) - se * qt[p] / pn);
   }
+  dq[i] = d;
 }
 
 // b[e] = sum_t dS[t][e] * s[t][e]
@@ -655,8 +654,8 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       double* A = w.take(static_cast<size_t>(P) * E);
       // enorm recomputed (cheap) with the forward's arithmetic
       cosine_enorm(P, E, w_score, en, st);
-      cosine_dq_kernel<<<(T + 127) / 128, 128, 0, st>>>(T, E, P, proj_out, w_score, en, scores, dS,
-                                                       dq, qn); ::fsmoe::count_launch();
+      cosine_dq_kernel<<<static_cast<int>((static_cast<long long>(T) * P + 255) / 256), 256, 0, st>>>(
+          T, E, P, proj_out, w_score, en, scores, dS, dq, qn); ::fsmoe::count_launch();
       cosine_b_kernel<<<E, 256, 0, st>>>(T, E, scores, dS, bb); ::fsmoe::count_launch();
       xtg(FSMOE_F64, T, P, E, qn, dS, E, 1, A, E, 1, 0, part, st);
       cosine_dw_kernel<<<(P * E + 255) / 256, 256, 0, st>>>(P, E, A, w_score, en, bb, dWs); ::fsmoe::count_launch();
