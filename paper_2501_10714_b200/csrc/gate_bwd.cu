@@ -126,7 +126,29 @@ __global__ void cosine_dw_kernel(int P, int E, const double* __restrict__ A,
   dW[i] += A[i] / wn - w[i] * b[e] / enorm[e];
 }
 
-constexpr int XT_TCH = 256;  // tokens per partial
+constexpr int XT_TCH = 256;  // tokens per partial (at most; fewer when that leaves SMs idle)
+
+// Tokens per partial chunk: 256, or fewer (a multiple of 32, at least 32) so
+// that chunks x column blocks gives the GPU two blocks per SM (small T, or a
+// narrow M such as the cosine projection's P rows).
+inline int xt_tch(int T, long long colblocks) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long long want = 2LL * sms;
+  const long long nch = (want + colblocks - 1) / colblocks;
+  long long tch = (T + nch - 1) / nch;
+  tch = (tch + 31) / 32 * 32;
+  return static_cast<int>(tch < 32 ? 32 : tch > XT_TCH ? XT_TCH : tch);
+}
+inline long long xt_chunks(int T, long long colblocks) {
+  const int tch = xt_tch(T, colblocks);
+  return (T + tch - 1) / tch;
+}
 constexpr int XT_J = 64;
 constexpr int XT_C = 16;
 
@@ -140,15 +162,15 @@ template <int DT, typename A>
 __global__ void __launch_bounds__(XT_J * XT_C)
     xtg_partial_kernel(int T, int M, int NC, const void* __restrict__ X,
                        const double* __restrict__ G, long long gst, long long gsc,
-                       double* __restrict__ part) {
+                       double* __restrict__ part, int tch) {
   __shared__ A xs[32][XT_J];
   __shared__ A gs[32][XT_C];
   const int chunk = blockIdx.z;
   const int j0 = blockIdx.x * XT_J, c0 = blockIdx.y * XT_C;
   const int jj = threadIdx.x % XT_J, cc = threadIdx.x / XT_J;
   A acc = A(0);
-  const int t_end = min(T, (chunk + 1) * XT_TCH);
-  for (int t0 = chunk * XT_TCH; t0 < t_end; t0 += 32) {
+  const int t_end = min(T, (chunk + 1) * tch);
+  for (int t0 = chunk * tch; t0 < t_end; t0 += 32) {
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * XT_J; i += XT_J * XT_C) {
       int tt = i / XT_J, j = i % XT_J;
@@ -221,15 +243,15 @@ __global__ void __launch_bounds__(256)
 template <int DT, typename A, int NCT>
 __global__ void __launch_bounds__(256)
     xtg2_kernel(int T, int M, int NC, const void* __restrict__ X, const double* __restrict__ G,
-                long long gst, long long gsc, double* __restrict__ part) {
+                long long gst, long long gsc, double* __restrict__ part, int tch) {
   __shared__ A gs[32][NCT];
   const int chunk = blockIdx.y;
   const int j = blockIdx.x * 256 + threadIdx.x;
   A acc[NCT];
 #pragma unroll
   for (int c = 0; c < NCT; ++c) acc[c] = A(0);
-  const int t_end = min(T, (chunk + 1) * XT_TCH);
-  for (int t0 = chunk * XT_TCH; t0 < t_end; t0 += 32) {
+  const int t_end = min(T, (chunk + 1) * tch);
+  for (int t0 = chunk * tch; t0 < t_end; t0 += 32) {
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * NCT; i += 256) {
       const int tt = i / NCT, c = i % NCT;
@@ -310,7 +332,7 @@ template <typename XT, int NCT2>
 __global__ void __launch_bounds__(256)
     xtg_pair_kernel(int T, int M, int NC, const XT* __restrict__ X, const double* __restrict__ G1,
                     const double* __restrict__ G2, long long gst, long long gsc,
-                    double* __restrict__ part) {
+                    double* __restrict__ part, int tch) {
   __shared__ __align__(16) float gs[32][NCT2];
   const int NC2 = G2 ? 2 * NC : NC;
   const int chunk = blockIdx.y;
@@ -318,8 +340,8 @@ __global__ void __launch_bounds__(256)
   float a0[NCT2], a1[NCT2];
 #pragma unroll
   for (int c = 0; c < NCT2; ++c) a0[c] = a1[c] = 0.f;
-  const int t_end = min(T, (chunk + 1) * XT_TCH);
-  for (int t0 = chunk * XT_TCH; t0 < t_end; t0 += 32) {
+  const int t_end = min(T, (chunk + 1) * tch);
+  for (int t0 = chunk * tch; t0 < t_end; t0 += 32) {
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * NCT2; i += 256) {
       const int tt = i / NCT2, c = i % NCT2;
@@ -471,11 +493,12 @@ struct Ws {
 template <int NCT>
 void xtg2_launch(int xdt, int T, int M, int NC, const void* X, const double* G, long long gst,
                  long long gsc, double* part, cudaStream_t st) {
-  dim3 grid((M + 255) / 256, (T + XT_TCH - 1) / XT_TCH);
+  const int tch = xt_tch(T, (M + 255) / 256);
+  dim3 grid((M + 255) / 256, (T + tch - 1) / tch);
   switch (xdt) {
-    case FSMOE_F64: xtg2_kernel<0, double, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
-    case FSMOE_F32: xtg2_kernel<1, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
-    default: xtg2_kernel<2, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part); break;
+    case FSMOE_F64: xtg2_kernel<0, double, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part, tch); break;
+    case FSMOE_F32: xtg2_kernel<1, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part, tch); break;
+    default: xtg2_kernel<2, float, NCT><<<grid, 256, 0, st>>>(T, M, NC, X, G, gst, gsc, part, tch); break;
   }
   ::fsmoe::count_launch();
 }
@@ -487,15 +510,16 @@ bool xtg_pair(int xdt, int T, int M, int NC, const void* X, const double* G1, co
               int accumulate, double* part, cudaStream_t st) {
   const int NC2 = G2 ? 2 * NC : NC;
   if (xdt == FSMOE_F64 || M % 2 || NC2 > 32) return false;
-  const int nchunks = (T + XT_TCH - 1) / XT_TCH;
+  const int tch = xt_tch(T, (M / 2 + 255) / 256);
+  const int nchunks = (T + tch - 1) / tch;
   dim3 grid((M / 2 + 255) / 256, nchunks);
   auto go = [&](auto nct) {
     constexpr int N = decltype(nct)::value;
     if (xdt == FSMOE_F32)
-      xtg_pair_kernel<float, N><<<grid, 256, 0, st>>>(T, M, NC, static_cast<const float*>(X), G1, G2, gst, gsc, part);
+      xtg_pair_kernel<float, N><<<grid, 256, 0, st>>>(T, M, NC, static_cast<const float*>(X), G1, G2, gst, gsc, part, tch);
     else
       xtg_pair_kernel<__nv_bfloat16, N><<<grid, 256, 0, st>>>(T, M, NC, static_cast<const __nv_bfloat16*>(X), G1,
-                                                                G2, gst, gsc, part);
+                                                                G2, gst, gsc, part, tch);
     ::fsmoe::count_launch();
   };
   if (NC2 <= 8) go(std::integral_constant<int, 8>{});
@@ -511,8 +535,8 @@ bool xtg_pair(int xdt, int T, int M, int NC, const void* X, const double* G1, co
 void xtg(int xdt, int T, int M, int NC, const void* X, const double* G, long long gst,
          long long gsc, double* out, long long osj, long long osc, int accumulate, double* part,
          cudaStream_t st) {
-  const int nchunks = (T + XT_TCH - 1) / XT_TCH;
   if (NC <= 64) {
+    const int nchunks = static_cast<int>(xt_chunks(T, (M + 255) / 256));
     if (NC <= 8) xtg2_launch<8>(xdt, T, M, NC, X, G, gst, gsc, part, st);
     else if (NC <= 16) xtg2_launch<16>(xdt, T, M, NC, X, G, gst, gsc, part, st);
     else if (NC <= 32) xtg2_launch<32>(xdt, T, M, NC, X, G, gst, gsc, part, st);
@@ -523,11 +547,14 @@ void xtg(int xdt, int T, int M, int NC, const void* X, const double* G, long lon
     ::fsmoe::count_launch();
     return;
   }
+  const long long cb = static_cast<long long>((M + XT_J - 1) / XT_J) * ((NC + XT_C - 1) / XT_C);
+  const int tch = xt_tch(T, cb);
+  const int nchunks = (T + tch - 1) / tch;
   dim3 grid((M + XT_J - 1) / XT_J, (NC + XT_C - 1) / XT_C, nchunks);
   switch (xdt) {
-    case FSMOE_F64: xtg_partial_kernel<0, double><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
-    case FSMOE_F32: xtg_partial_kernel<1, float><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
-    default: xtg_partial_kernel<2, float><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part); ::fsmoe::count_launch(); break;
+    case FSMOE_F64: xtg_partial_kernel<0, double><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part, tch); ::fsmoe::count_launch(); break;
+    case FSMOE_F32: xtg_partial_kernel<1, float><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part, tch); ::fsmoe::count_launch(); break;
+    default: xtg_partial_kernel<2, float><<<grid, XT_J * XT_C, 0, st>>>(T, M, NC, X, G, gst, gsc, part, tch); ::fsmoe::count_launch(); break;
   }
   long long n = static_cast<long long>(M) * NC;
   xtg_reduce_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(nchunks, M, NC, part, out,
@@ -588,14 +615,32 @@ void dx_acc(int xdt, int T, int M, int NC, const double* G, long long gst, long 
 
 }  // namespace
 
+// Partial-sum elements the largest x^T G of a gate backward needs: every
+// (rows, columns) contraction it may run (rows M or P; columns E, 2E paired,
+// or P) with the chunking its kernel would pick.
+size_t xt_part_elems(int T, int M, int E, int P) {
+  size_t best = 1;
+  auto consider = [&](int rows, int nc2) {
+    if (rows <= 0 || nc2 <= 0) return;
+    const long long cbs[3] = {(rows / 2 + 255) / 256, (rows + 255) / 256,
+                              static_cast<long long>((rows + XT_J - 1) / XT_J) * ((nc2 + XT_C - 1) / XT_C)};
+    for (long long cb : cbs) {
+      const size_t n = static_cast<size_t>(xt_chunks(T, cb < 1 ? 1 : cb)) * rows * nc2;
+      if (n > best) best = n;
+    }
+  };
+  consider(M, 2 * E);
+  consider(M, P);
+  consider(P, E);
+  return best;
+}
+
 size_t gate_bwd_workspace_bytes(const fsmoe_gate_desc& d) {
   const size_t T = d.tokens, E = d.score_cols, M = d.model_dim, P = d.proj_rows > 0 ? d.proj_rows : 0;
-  const size_t nch = (T + XT_TCH - 1) / XT_TCH;
-  size_t nc = E > P ? E : P;
-  size_t wide = M > P ? M : P;
   auto r = [](size_t n) { return (n * 8 + 255) & ~size_t(255); };
-  // partials hold two column groups (xtg_pair: the noisy gate's dS | dZ)
-  return r(T * E) * 2 + r(T * P) * 2 + r(nch * wide * 2 * (nc > 0 ? nc : 1)) + r(P * E) + r(E) * 2 + 1024;
+  return r(T * E) * 2 + r(T * P) * 2 + r(xt_part_elems(static_cast<int>(T), static_cast<int>(M),
+                                                        static_cast<int>(E), static_cast<int>(P))) +
+         r(P * E) + r(E) * 2 + 1024;
 }
 
 int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
@@ -612,10 +657,8 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
   if (softmax_gate && k == 1) return FSMOE_OK;
   Ws w{static_cast<char*>(ws)};
   double* dS = w.take(static_cast<size_t>(T) * E);
-  const int nch = (T + XT_TCH - 1) / XT_TCH;
   const int P = d.proj_rows > 0 ? d.proj_rows : 0;
-  const int nc = E > P ? E : P;
-  double* part = w.take(static_cast<size_t>(nch) * (M > P ? M : P) * 2 * (nc > 0 ? nc : 1));
+  double* part = w.take(xt_part_elems(T, M, E, P));
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
       dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
