@@ -244,7 +244,7 @@ template <int DT, typename A, int NCT>
 __global__ void __launch_bounds__(256)
     xtg2_kernel(int T, int M, int NC, const void* __restrict__ X, const double* __restrict__ G,
                 long long gst, long long gsc, double* __restrict__ part, int tch) {
-  __shared__ A gs[32][NCT];
+  __shared__ __align__(16) A gs[32][NCT];
   const int chunk = blockIdx.y;
   const int j = blockIdx.x * 256 + threadIdx.x;
   A acc[NCT];
@@ -261,10 +261,18 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (j < M) {
       const int nt = min(32, t_end - t0);
-      for (int tt = 0; tt < nt; ++tt) {
-        const A xv = static_cast<A>(load_as_double<DT>(X, static_cast<long long>(t0 + tt) * M + j));
+      for (int u0 = 0; u0 < nt; u0 += 8) {  // eight tokens' x loads in flight
+        A xv[8];
 #pragma unroll
-        for (int c = 0; c < NCT; ++c) acc[c] += xv * gs[tt][c];
+        for (int u = 0; u < 8; ++u)
+          xv[u] = u0 + u < nt ? static_cast<A>(load_as_double<DT>(X, static_cast<long long>(t0 + u0 + u) * M + j))
+                              : A(0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u0 + u >= nt) break;
+#pragma unroll
+          for (int c = 0; c < NCT; ++c) acc[c] += xv[u] * gs[u0 + u][c];
+        }
       }
     }
   }
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(256)
     dx_acc2_kernel(int Tn, int M, int NC, const double* __restrict__ G1, const double* __restrict__ W1,
                    const double* __restrict__ G2, const double* __restrict__ W2, long long gst,
                    long long gsc, long long wsj, long long wsc, T* __restrict__ dx) {
-  __shared__ A gs[2][32][NCT];
+  __shared__ __align__(16) A gs[2][32][NCT];
   const int j = blockIdx.x * 256 + threadIdx.x;
   const int t0 = blockIdx.y * 32;
   const int npj = G2 ? 2 : 1;
@@ -298,16 +306,25 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   if (j >= M) return;
-  for (int tt = 0; tt < 32 && t0 + tt < Tn; ++tt) {
-    A a = A(0);
+  const int nt = min(32, Tn - t0);
+  for (int u0 = 0; u0 < nt; u0 += 8) {  // eight tokens' dx loads in flight
+    T dv[8];
 #pragma unroll
-    for (int c = 0; c < NCT; ++c) a += gs[0][tt][c] * w1[c];
-    if (G2)
+    for (int u = 0; u < 8; ++u) dv[u] = u0 + u < nt ? dx[static_cast<long long>(t0 + u0 + u) * M + j] : T(0);
 #pragma unroll
-      for (int c = 0; c < NCT; ++c) a += gs[1][tt][c] * w2[c];
-    T* p = dx + static_cast<long long>(t0 + tt) * M + j;
-    if constexpr (sizeof(T) == 2) *p = __float2bfloat16(__bfloat162float(*p) + static_cast<float>(a));
-    else *p = static_cast<T>(static_cast<double>(*p) + static_cast<double>(a));
+    for (int u = 0; u < 8; ++u) {
+      if (u0 + u >= nt) break;
+      const int tt = u0 + u;
+      A a = A(0);
+#pragma unroll
+      for (int c = 0; c < NCT; ++c) a += gs[0][tt][c] * w1[c];
+      if (G2)
+#pragma unroll
+        for (int c = 0; c < NCT; ++c) a += gs[1][tt][c] * w2[c];
+      T* p = dx + static_cast<long long>(t0 + tt) * M + j;
+      if constexpr (sizeof(T) == 2) *p = __float2bfloat16(__bfloat162float(dv[u]) + static_cast<float>(a));
+      else *p = static_cast<T>(static_cast<double>(dv[u]) + static_cast<double>(a));
+    }
   }
 }
 
