@@ -27,6 +27,7 @@
 #include <type_traits>
 
 #include "capi_common.h"
+#include "host_once.h"
 #include "kernels.h"
 #include "route_common.cuh"
 
@@ -350,15 +351,16 @@ void launch_select(cudaStream_t st, int T, int E, int k, uint64_t seed, const do
                    const double* spread, int P, const double* w_score, const double* enorm,
                    int* pt, int* pe, double* pw, double* scores_out, double* noise_out,
                    int* status) {
-  const int blocks = (T + 127) / 128;
+  const int tpb = per_token_block(T);
+  const int blocks = (T + tpb - 1) / tpb;
   if (E <= 16)
-    token_select_kernel<KIND, 16><<<blocks, 128, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
+    token_select_kernel<KIND, 16><<<blocks, tpb, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
                                                           enorm, pt, pe, pw, scores_out, noise_out, status);
   else if (E <= 64)
-    token_select_kernel<KIND, 64><<<blocks, 128, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
+    token_select_kernel<KIND, 64><<<blocks, tpb, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
                                                           enorm, pt, pe, pw, scores_out, noise_out, status);
   else
-    token_select_kernel<KIND, 256><<<blocks, 128, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
+    token_select_kernel<KIND, 256><<<blocks, tpb, 0, st>>>(T, E, k, seed, raw, spread, P, w_score,
                                                            enorm, pt, pe, pw, scores_out, noise_out, status);
   ::fsmoe::count_launch();
 }

@@ -13,6 +13,7 @@
 #include <type_traits>
 
 #include "capi_common.h"
+#include "host_once.h"
 #include "kernels.h"
 #include "route_common.cuh"
 
@@ -678,7 +679,7 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
   double* part = w.take(xt_part_elems(T, M, E, P));
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
-      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
+      dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dZ = w.take(static_cast<size_t>(T) * E);
       long long n = static_cast<long long>(T) * E;
       noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ); ::fsmoe::count_launch();
@@ -693,7 +694,7 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       break;
     }
     case FSMOE_GATE_SIGMOID_TOPK: {
-      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(1, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
+      dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(1, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       if (!xtg_pair(d.x_dtype, T, M, E, x, dS, nullptr, E, 1, dWs, nullptr, E, 1, 1, part, st))
         xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
       dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);
@@ -706,7 +707,7 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       break;
     }
     case FSMOE_GATE_COSINE_TOPK: {
-      dscore_token_kernel<<<(T + 127) / 128, 128, 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
+      dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dq = w.take(static_cast<size_t>(T) * P);
       double* qn = w.take(static_cast<size_t>(T) * P);
       double* en = w.take(E);

@@ -1296,9 +1296,9 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
   }
   ::fsmoe::count_launch();
   if (noisy) {
-    if (E <= 16) mt_kernel<16><<<(T + 127) / 128, 128, 0, st>>>(T, E, d.seed, w.draws);
-    else if (E <= 32) mt_kernel<32><<<(T + 127) / 128, 128, 0, st>>>(T, E, d.seed, w.draws);
-    else mt_kernel<64><<<(T + 127) / 128, 128, 0, st>>>(T, E, d.seed, w.draws);
+    if (E <= 16) mt_kernel<16><<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(T, E, d.seed, w.draws);
+    else if (E <= 32) mt_kernel<32><<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(T, E, d.seed, w.draws);
+    else mt_kernel<64><<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(T, E, d.seed, w.draws);
     ::fsmoe::count_launch();
   }
   // |s~ - s_ref| <= cB |x| |w|: fp32 rounding of x, w and the M-term FMA chain
@@ -1314,7 +1314,7 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
     bound_kernel<1><<<pb, 256, 0, st>>>(T, E, M, w.part, w.xn2, w.wn, cB, w.draws, w.noise, w.sapx,
                                         w.spapx, w.lo, w.hi);
   ::fsmoe::count_launch();
-  cand_kernel<<<(T + 127) / 128, 128, 0, st>>>(T, E, k, w.lo, w.hi, w.mask, w.lists, w.counts);
+  cand_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(T, E, k, w.lo, w.hi, w.mask, w.lists, w.counts);
   ::fsmoe::count_launch();
   const PruneWsView v{w.WT, w.lists, w.counts, w.s_exact, w.sp_exact};
   switch (d.x_dtype * 2 + (noisy ? 0 : 1)) {
