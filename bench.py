@@ -130,6 +130,14 @@ class ClockSampler:
             for n, v in zip(names, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
+            try:  # the full event-reason mask (nvml bit order) for the rest
+                mask = int(parts[4], 16)
+            except ValueError:
+                mask = 0
+            for bit, n in ((0x1, "gpu_idle"), (0x2, "applications_clocks_setting"), (0x10, "sync_boost"),
+                           (0x80, "hw_power_brake_slowdown"), (0x100, "display_clock_setting")):
+                if mask & bit:
+                    reasons.add(n)
         os.unlink(self.path)
         if sm:
             out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons),
