@@ -1,0 +1,60 @@
+"""bench.py host logic on CPU: the trace timeline summary (exposed comm time),
+the nvidia-smi clock sampler's parsing and the workload table the JSON
+contract names."""
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def test_timeline_summary_exposed_comm():
+    # comm [0, 10) us and [20, 30) us; compute covers [5, 25) us -> exposed 5 + 5
+    ev = [{"name": "fwd.dispatch", "tid": 0, "ts": 0.0, "dur": 10.0},
+          {"name": "fwd.combine", "tid": 0, "ts": 20.0, "dur": 10.0},
+          {"name": "fwd.expert[0]", "tid": 2, "ts": 5.0, "dur": 20.0}]
+    out = bench.timeline_summary(json.dumps({"traceEvents": ev}), steps=1)
+    assert out["comm_exposed_ms_per_step"] == pytest.approx(0.010)
+    assert out["comm_ms_per_step"] == pytest.approx(0.020)
+    assert out["phase_ms_per_step"]["fwd.expert"] == pytest.approx(0.020)
+    assert out["traced_ms_per_step"] == pytest.approx(0.030)
+
+
+def test_clock_sampler_parses_region_samples(tmp_path):
+    s = bench.ClockSampler(0)
+    s.path = str(tmp_path / "clk.csv")
+    rows = [
+        "0, 1965, 1965, 200.0, 0x0000000000000001, Not Active, Not Active, Not Active, Not Active",  # idle, before
+        "0, 1800, 1965, 990.0, 0x0000000000000004, Not Active, Not Active, Not Active, Active",
+        "0, 1700, 1965, 995.0, 0x0000000000000014, Not Active, Not Active, Not Active, Active",
+        "0, 1965, 1965, 700.0, 0x0000000000000000, Not Active, Not Active, Not Active, Not Active",
+    ]
+    with open(s.path, "w") as f:
+        f.write("\n".join(rows) + "\n")
+    s.n0 = 1  # the first line was written before the timed region
+
+    class Done:  # stands in for the finished nvidia-smi process
+        def terminate(self):
+            pass
+
+        def wait(self, timeout=None):
+            return 0
+
+    s.proc = Done()
+    out = s.stop()
+    assert out["samples"] == 3
+    assert out["sm_mhz"] == 1800.0
+    assert out["sm_max_mhz"] == 1965.0
+    assert out["reasons"] == ["sw_power_cap", "sync_boost"]
+
+
+def test_workloads_table():
+    assert bench.WORKLOADS["gpt2m"]["tokens_per_gpu"] == 16384
+    assert bench.WORKLOADS["mixtral"]["d_ffn"] == 14336
+    assert set(bench.GATES) == {"noisy_topk", "sigmoid_topk", "cosine_topk", "expert_choice"}
+    for w in bench.WORKLOADS.values():
+        assert {"workload", "tokens_per_gpu", "d_model", "d_ffn", "experts", "top_k"} <= set(w)
