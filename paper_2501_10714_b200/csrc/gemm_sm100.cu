@@ -242,12 +242,29 @@ struct EpiMaps {
 
 template <int CTAS>
 __device__ __forceinline__ TileInfo decode_tile_c(const KParams& p, int t) {
+  // Tile order inside a group: bands of TILE_GM m-tiles, walked column by
+  // column (m fastest), so the tiles in flight at once share a few A row
+  // blocks and B column blocks that stay in L2 -- with m-major order every
+  // m-tile streamed the whole B (a 235 MB Mixtral W1) again from HBM.
+  // Only for wide problems (n-tiles > 2 bands): with few n-tiles the m-major
+  // order already keeps the whole B in flight, and banding measured worse
+  // there (ncu dram reads of the N = 4096 launches grew 1.4-2x).
+  constexpr int TILE_GM = 8;
   TileInfo ti;
   int per_g = p.m_tiles * p.n_tiles;
   ti.g = t / per_g;
   int rem = t - ti.g * per_g;
-  ti.mt = rem / p.n_tiles;
-  ti.nt = rem - ti.mt * p.n_tiles;
+  if (p.m_tiles >= 2 * TILE_GM && p.n_tiles > 2 * TILE_GM) {
+    const int band = rem / (TILE_GM * p.n_tiles);
+    const int m0 = band * TILE_GM;
+    const int gm = min(TILE_GM, p.m_tiles - m0);
+    const int idx = rem - band * TILE_GM * p.n_tiles;
+    ti.mt = m0 + idx % gm;
+    ti.nt = idx / gm;
+  } else {
+    ti.mt = rem / p.n_tiles;
+    ti.nt = rem - ti.mt * p.n_tiles;
+  }
   ti.skip = p.kind == 0 &&
             (ti.mt * TileCfg<CTAS>::BM >= valid_of(p, ti.g) || !fsmoe_dev::in_range(p.blocks, ti.g));
   return ti;
