@@ -252,12 +252,14 @@ __global__ void __launch_bounds__(32)
                          const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
                          const uint8_t* __restrict__ x, const PeerRows buf, const RowRange rr) {
   extern __shared__ __align__(128) uint8_t sm[];  // [BK_ROWS][row_bytes] + one zero row
-  __shared__ __align__(8) uint64_t bar;
+  // one mbarrier per lane: a row's store leaves as soon as that row has landed
+  // instead of after the whole group of BK_ROWS rows
+  __shared__ __align__(8) uint64_t bar[BK_ROWS];
   const int lane = threadIdx.x;
   uint8_t* zero = sm + BK_ROWS * row_bytes;
   for (int i = lane * 16; i < row_bytes; i += 32 * 16) *reinterpret_cast<uint4*>(zero + i) = make_uint4(0, 0, 0, 0);
-  if (lane == 0) {
-    fsmoe_dev::mbar_init(&bar, 32);
+  if (lane < BK_ROWS) {
+    fsmoe_dev::mbar_init(&bar[lane], 1);
     fsmoe_dev::fence_barrier_init();
   }
   fsmoe_dev::fence_proxy_async_smem();  // the zero row (generic writes) -> async proxy
@@ -268,26 +270,23 @@ __global__ void __launch_bounds__(32)
   // persistent: a block walks groups of BK_ROWS slots (lanes >= BK_ROWS idle)
   for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const long long s = g * BK_ROWS + lane;
-    int p = -1;
     const bool valid = lane < BK_ROWS && s < n_slots && in_range(rr, s);
-    if (valid) p = pick_of_slot[s];
+    const int p = valid ? pick_of_slot[s] : -1;
     if (p >= 0) {
-      fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
-      fsmoe_dev::bulk_load(mine, x + static_cast<long long>(ptok[p]) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
-    } else {
-      fsmoe_dev::mbar_arrive(&bar);
+      fsmoe_dev::mbar_arrive_expect_tx(&bar[lane], static_cast<uint32_t>(row_bytes));
+      fsmoe_dev::bulk_load(mine, x + static_cast<long long>(ptok[p]) * row_bytes, static_cast<uint32_t>(row_bytes), &bar[lane]);
+      fsmoe_dev::mbar_wait(&bar[lane], phase);
+      phase ^= 1u;
     }
-    fsmoe_dev::mbar_wait(&bar, phase);
-    phase ^= 1u;
     if (valid) {
       char* dst = peer_row(buf, slot_row(s, E, C, chunks), row_bytes);
       bulk_store(dst, p >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
       fsmoe_dev::bulk_commit();
     }
-    fsmoe_dev::bulk_wait_read<0>();  // the row buffer is free for the next group
-    __syncwarp();
+    fsmoe_dev::bulk_wait_read<0>();  // this lane's row buffer is free for the next group
   }
   fsmoe_dev::bulk_wait<0>();  // shared memory must outlive the stores
+  __syncwarp();
 }
 
 // dst[i] = src[idx[i]] (idx < 0: zero row), i < n_rows, through the TMA
@@ -298,12 +297,12 @@ __global__ void __launch_bounds__(32)
     gather_bulk_kernel(long long n_rows, int row_bytes, const int* __restrict__ idx,
                        const uint8_t* __restrict__ src, const PeerRows dst) {
   extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar[BK_ROWS];  // one per lane, as in dispatch_bulk_kernel
   const int lane = threadIdx.x;
   uint8_t* zero = sm + BK_ROWS * row_bytes;
   for (int b = lane * 16; b < row_bytes; b += 32 * 16) *reinterpret_cast<uint4*>(zero + b) = make_uint4(0, 0, 0, 0);
-  if (lane == 0) {
-    fsmoe_dev::mbar_init(&bar, 32);
+  if (lane < BK_ROWS) {
+    fsmoe_dev::mbar_init(&bar[lane], 1);
     fsmoe_dev::fence_barrier_init();
   }
   fsmoe_dev::fence_proxy_async_smem();
@@ -316,21 +315,19 @@ __global__ void __launch_bounds__(32)
     const bool valid = lane < BK_ROWS && i < n_rows;
     const int s = valid ? idx[i] : -1;
     if (s >= 0) {
-      fsmoe_dev::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(row_bytes));
-      fsmoe_dev::bulk_load(mine, src + static_cast<long long>(s) * row_bytes, static_cast<uint32_t>(row_bytes), &bar);
-    } else {
-      fsmoe_dev::mbar_arrive(&bar);
+      fsmoe_dev::mbar_arrive_expect_tx(&bar[lane], static_cast<uint32_t>(row_bytes));
+      fsmoe_dev::bulk_load(mine, src + static_cast<long long>(s) * row_bytes, static_cast<uint32_t>(row_bytes), &bar[lane]);
+      fsmoe_dev::mbar_wait(&bar[lane], phase);
+      phase ^= 1u;
     }
-    fsmoe_dev::mbar_wait(&bar, phase);
-    phase ^= 1u;
     if (valid) {
       bulk_store(peer_row(dst, i, row_bytes), s >= 0 ? mine : zero, static_cast<uint32_t>(row_bytes));
       fsmoe_dev::bulk_commit();
     }
     fsmoe_dev::bulk_wait_read<0>();
-    __syncwarp();
   }
   fsmoe_dev::bulk_wait<0>();
+  __syncwarp();
 }
 
 // persistent grid for the bulk row movers: every resident block slot, at
