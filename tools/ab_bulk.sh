@@ -1,3 +1,7 @@
+# Same-box A/B of two libfsmoe_cuda.so builds: the current build vs the one
+# copied to _oldlib/libfsmoe_cuda_old.so (git-ignored; travels with gpurun).
+# Runs pytest -m gpu on the current build, alternates bench.py runs, and takes
+# an ncu duration/DRAM list of the row movers for each build.
 set -x
 L=paper_2501_10714_b200/lib
 cp $L/libfsmoe_cuda.so _oldlib/new.so
