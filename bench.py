@@ -4,12 +4,16 @@
 Headline (BASELINE.json "metric"): MoE layer fwd+bwd tokens/sec at 1/2/4/8
 B200 and the fraction of the GEMM / NVLink roofline.
 
-Workload (BASELINE configs[1], the GPT-2-medium shape): per GPU 16384 tokens,
-d_model 1024, d_ffn 4096 (simple FFN, GELU), 16 experts top-1 Switch routing
-(the reference's noisy_topk with k=1: combine weight exactly 1.0), capacity
-factor 1.0 (C = 1024 per expert and rank), bf16 activations / expert weights
-with fp32 accumulation, fp64-exact gate. N GPUs = expert parallel over N ranks
-(16/N experts each), tokens per GPU fixed (weak scaling).
+Workload (default: BASELINE configs[2], the north-star Mixtral-8x7B shape):
+per GPU 32768 tokens, d_model 4096, d_ffn 14336 SwiGLU (3 GEMMs), 8 experts
+top-2 GShard routing (the reference's noisy_topk, k = 2), capacity factor 1.0
+(C = 8192 per expert and rank), bf16 activations / expert weights with fp32
+accumulation, fp64-exact gate. N GPUs = expert parallel over N ranks (8/N
+experts each; N = 8 is one expert per GPU, N = 1 runs all 8 experts locally,
+i.e. the same per-GPU expert work as the 8-GPU job), tokens per GPU fixed
+(weak scaling). `--config gpt2m` runs configs[1] (GPT-2-medium shape, 16
+experts top-1 Switch), `--config gpt2xl --gate G` SURVEY C5; the default run
+also measures configs[1] at the same N as an extra key.
 
 A step = gate -> order -> AlltoAll -> expert FFN -> AlltoAll -> I-order and
 the full backward (expert dgrad + wgrad, combine/dispatch backward, gate
@@ -54,7 +58,7 @@ WORKLOADS = {
                    capacity_factor=1.0, dtype="bf16 / fp32 accumulate",
                    l2="weights + activations ~0.3 GB per step (> L2): no flush needed"),
 }
-WORKLOAD = WORKLOADS["gpt2m"]
+WORKLOAD = WORKLOADS["mixtral"]
 GATES = ("noisy_topk", "sigmoid_topk", "cosine_topk", "expert_choice")
 NVLINK_GBS = 900.0  # nominal per direction per GPU (measured peer copy ~770)
 
@@ -147,78 +151,112 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline --
 
-def cpu_reference_rate(seconds: float, threads: int, tokens_per_call: int, x, w_gate, w_noise,
-                       experts: int, capacity_per_call: int):
+def cpu_threads_for(T, M, E, cap):
+    """Threads that can each run one full routing instance at once: every
+    reference call holds about x + 2 buffers + y in fp64 plus its copies
+    (≈ 2.5·(E·C + T)·M·8 bytes); use at most 60 % of the available memory."""
+    per = 2.5 * (E * cap + T) * M * 8
+    avail = None
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    avail = int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    cores = os.cpu_count() or 1
+    if not avail:
+        return 1
+    return int(max(1, min(cores, (0.6 * avail) // per)))
+
+
+def cpu_reference_pass(threads, x, w_gate, w_noise, experts, top_k, capacity):
     """The reference's own implementation of the path (run_gate -> dispatch_tokens
-    -> combine_tokens, fp64, identity experts; proj/src/workload.cpp:143-282) on
-    host cores: oracle/_ref (compiled from /root/reference) when present, else
-    the C restatement. One call per thread on its own token shard, repeated
-    until `seconds` elapse. Returns (tokens/s, kind, threads, calls)."""
+    -> combine_tokens, fp64, identity experts; proj/src/workload.cpp:143-282)
+    on host cores, over the SAME routing instance the GPU arm runs (all T
+    tokens of one rank, capacity C): oracle/_ref (compiled from
+    /root/reference) when present, else the C restatement. Every thread runs
+    the whole instance once (the reference is serial per call; threads add
+    throughput, not a split of the instance, which would change the capacity
+    semantics). Returns (tokens/s, kind, threads, wall seconds)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
     kind = "reference" if pyoracle.available("reference") else "port"
     orcs = [pyoracle.Oracle(kind) for _ in range(threads)]
-    done = [0] * threads
-    stop = [False]
+    errs = []
 
     def work(i):
-        o = orcs[i]
-        while not stop[0]:
-            xs = x[(i * tokens_per_call) % x.shape[0]:][:tokens_per_call]
-            g = o.run_gate("noisy_topk", WORKLOAD["top_k"], 7, xs, w_gate, w_noise)
-            d = o.dispatch(xs, experts, g.token, g.expert, capacity_per_call)
-            o.combine(d.buffers, xs.shape[0], experts, g.token, g.expert, g.weight, d.slot_of_pick,
-                      xs.shape[1])
-            done[i] += 1
+        try:
+            o = orcs[i]
+            g = o.run_gate("noisy_topk", top_k, 7, x, w_gate, w_noise)
+            d = o.dispatch(x, experts, g.token, g.expert, capacity)
+            o.combine(d.buffers, x.shape[0], experts, g.token, g.expert, g.weight, d.slot_of_pick,
+                      x.shape[1])
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
 
     ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
     t0 = time.perf_counter()
     for t in ts:
         t.start()
-    time.sleep(seconds)
-    stop[0] = True
     for t in ts:
         t.join()
     wall = time.perf_counter() - t0
-    calls = sum(done)
-    return calls * tokens_per_call / wall, kind, threads, calls, wall
+    if errs:
+        raise errs[0]
+    return threads * x.shape[0] / wall, kind, threads, wall
 
 
 def cpu_inputs(tokens, M, E, seed=1):
+    """The routing instance on the host: x (bf16 values, upcast to fp64, as the
+    GPU arm's tokens), score and noise weights U(-1/sqrt(M), 1/sqrt(M))."""
     import numpy as np
-    rng = np.random.default_rng(seed)
     import torch
-    x = torch.from_numpy(rng.uniform(-1, 1, (tokens, M))).to(torch.bfloat16).double().numpy()
+    rng = np.random.default_rng(seed)
+    x = torch.from_numpy(rng.standard_normal((tokens, M), dtype=np.float32)).to(torch.bfloat16)
+    x = x.double().numpy()
     wg = rng.uniform(-1, 1, (M, E)) / np.sqrt(M)
     wn = rng.uniform(-1, 1, (M, E)) / np.sqrt(M)
     return x, wg, wn
 
 
+def instance_capacity():
+    """capacity_tokens (workload.cpp:43-51) of the GPU arm's per-rank instance."""
+    import math
+    W = WORKLOAD
+    return int(math.ceil(W["top_k"] * W["capacity_factor"] * W["tokens_per_gpu"] / W["experts"] - 1e-9))
+
+
 def reference_arm(args):
-    """--impl reference: the reference's CPU implementation of the path, timed
-    with all host threads on this workload's shape, one bounded sample/step."""
-    M, E, T = WORKLOAD["d_model"], WORKLOAD["experts"], 1024
-    threads = os.cpu_count() or 1
-    x, wg, wn = cpu_inputs(T * threads, M, E)
-    cap = -(-T * WORKLOAD["top_k"] // E)  # capacity_tokens(k, f=1.0) for the sample's B*L
-    for _ in range(args.warmup):
-        cpu_reference_rate(0.2, threads, T, x, wg, wn, E, cap)
+    """--impl reference: the reference's CPU implementation of the path on the
+    GPU arm's routing instance (T tokens, capacity C), all the threads the
+    host's memory allows, each step = every thread routing the full instance."""
+    M, E, T, k = WORKLOAD["d_model"], WORKLOAD["experts"], WORKLOAD["tokens_per_gpu"], WORKLOAD["top_k"]
+    cap = instance_capacity()
+    threads = cpu_threads_for(T, M, E, cap)
+    x, wg, wn = cpu_inputs(T, M, E)
+    # CPU warm-up: one pass (page-in, allocator); the GPU arm's W >= 3 rule is
+    # about clocks and caches that a CPU pass does not have
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference_pass(threads, x, wg, wn, E, k, cap)
     rates, walls, kind = [], [], "port"
     for _ in range(args.steps):
-        r, kind, thr, calls, wall = cpu_reference_rate(1.0, threads, T, x, wg, wn, E, cap)
+        r, kind, thr, wall = cpu_reference_pass(threads, x, wg, wn, E, k, cap)
         rates.append(r)
-        walls.append(wall * 1e3 / max(calls / threads, 1))
+        walls.append(wall * 1e3)
     value = statistics.median(rates)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
         "ms_per_step": statistics.median(walls), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(WORKLOAD, reference_path="run_gate -> dispatch_tokens -> combine_tokens "
+        "config": dict(WORKLOAD, capacity=cap,
+                       reference_path="run_gate -> dispatch_tokens -> combine_tokens "
                        "(the reference has no expert FFN and no backward)"),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
-                         "sample": f"{threads} threads x {T} tokens per call, d_model {M}, "
-                                   f"{E} experts, top-{WORKLOAD['top_k']}, ~1 s per step"},
+                         "sample": f"{threads} threads, each routing the GPU arm's full instance "
+                                   f"(T {T}, d_model {M}, {E} experts, top-{k}, capacity {cap}) "
+                                   "once per step"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -276,14 +314,23 @@ def gemm_roofline(layer, peaks, reps=5):
     flops = sum(v[0] for v in per.values())
     ms = sum(v[1] for v in per.values())
     achieved = flops / (ms * 1e-3) / 1e12
-    peak = peaks.get("bf16_tflops", 1590.0)
+    # MEASURED_PEAKS.json: the burst cuBLAS figure for a kernel timed alone
+    # (short), the sustained (4 s back-to-back) one when the timed GEMMs run
+    # for tens of milliseconds, i.e. power-capped like the step itself
+    sustained = ms * reps >= 50.0
+    peak = peaks.get("bf16_tflops_sustained" if sustained else "bf16_tflops", 1590.0)
+    epi = "SwiGLU" if cfg.ffn == "gated3" else "GELU"
     return {
         "bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
         "frac": round(achieved / peak, 4), "traffic": None,
-        "kernel": "grouped_gemm_kernel (tcgen05 cta_group::2; 6 launches/step: fwd1 (256x256 tiles, GELU) fwd2 wgrad2 (256x512) dgrad2 (256x256, GELU bwd) wgrad1 dgrad1 (256x512))",
+        "frac_vs_burst": round(achieved / peaks.get("bf16_tflops", 1590.0), 4),
+        "kernel": f"grouped_gemm_kernel (tcgen05 cta_group::2; 6 launches/step: fwd1 ({epi} epilogue), "
+                  f"fwd2, wgrad2, dgrad2 ({epi} backward epilogue), wgrad1, dgrad1)",
         "flops_per_step": flops, "gemm_ms_per_step": round(ms, 4),
         "per_launch_ms": {k: round(v[1], 4) for k, v in per.items()},
-        "peak_kind": "bf16_tflops (burst) of MEASURED_PEAKS.json",
+        "peak_kind": ("bf16_tflops_sustained" if sustained else "bf16_tflops (burst)")
+                     + f" of MEASURED_PEAKS.json ({reps} back-to-back reps per launch = "
+                       f"{ms * reps:.0f} ms of GEMMs)",
     }, flops, ms
 
 
@@ -314,46 +361,48 @@ def timeline_summary(trace: str, steps: int):
             "note": "traced run synchronises per phase call; shares, not absolute step time"}
 
 
-def gpu_arm(args):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-    from paper_2501_10714_b200 import _native
-    from paper_2501_10714_b200.layer import EpGroup, MoEConfig, MoELayer
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    peaks, peak_kind = load_peaks()
-    T, M, H, E = (WORKLOAD["tokens_per_gpu"], WORKLOAD["d_model"], WORKLOAD["d_ffn"],
-                  WORKLOAD["experts"])
-    gate = args.gate or WORKLOAD["gate"].split()[0]
+def make_layer(W, args, world, rank, ep, gate=None):
+    from paper_2501_10714_b200.layer import MoEConfig, MoELayer
+    gate = gate or W["gate"].split()[0]
     # expert choice: every expert takes C = k f T / E tokens (workload.cpp:156-171,
     # the layer derives C from k); cosine: a 64-row projection (the reference
     # leaves the dimension open)
-    cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=WORKLOAD["top_k"], gate=gate, ffn=WORKLOAD["ffn"].split()[0], capacity_factor=1.0,
-                    proj_dim=64 if gate == "cosine_topk" else 0,
+    cfg = MoEConfig(tokens=W["tokens_per_gpu"], model_dim=W["d_model"], ffn_dim=W["d_ffn"],
+                    experts=W["experts"], top_k=W["top_k"], gate=gate, ffn=W["ffn"].split()[0],
+                    capacity_factor=W["capacity_factor"], proj_dim=64 if gate == "cosine_topk" else 0,
                     precision="bf16", seed=7, r_fwd=args.r_fwd, r_bwd=args.r_bwd)
-    ep = EpGroup(world, rank, local, max_ctas=args.nccl_ctas) if world > 1 else None
-    layer = MoELayer(cfg, ep, init_seed=1)
-    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    x = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
-    dy = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
-    dx = torch.empty_like(x)
-    y = torch.empty_like(x)
+    return MoELayer(cfg, ep, init_seed=1)
+
+
+def timed_steps(layer, x, y, dy, dx, args, world, warm_seconds):
+    """W warm-up steps, then more until `warm_seconds` of steady stepping have
+    passed (clocks settle under the power cap), then EXACTLY args.steps timed
+    steps between barriers + synchronize, CUDA events on the launching stream,
+    max over ranks. Returns (ms/step, extra warm-up steps, clocks, launches,
+    exposed-wait ms/step of this rank)."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    from paper_2501_10714_b200 import _native
     for _ in range(args.warmup):
         layer.forward(x, y)
         layer.backward(dy, dx)
     torch.cuda.synchronize()
+    extra = 0
+    t_end = time.perf_counter() + warm_seconds
+    while time.perf_counter() < t_end:
+        layer.forward(x, y)
+        layer.backward(dy, dx)
+        torch.cuda.synchronize()
+        extra += 1
     if world > 1:
         dist.barrier()
     lib = _native.cuda_lib()
-    lib.fsmoe_launch_count.restype = __import__("ctypes").c_longlong
-    clocks = ClockSampler(local)
+    lib.fsmoe_launch_count.restype = ctypes.c_longlong
+    wait_buf = layer.buffer("wait_ns", torch.int64) if world > 1 else None
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clocks.start()
+    w0 = int(layer.buffer("wait_ns", torch.int64).item()) if world > 1 else 0
     n0 = lib.fsmoe_launch_count()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -370,40 +419,79 @@ def gpu_arm(args):
         dist.barrier()
     clk = clocks.stop()
     ms = s.elapsed_time(e) / args.steps
+    wait_ms = 0.0
+    if wait_buf is not None:
+        wait_ms = (int(layer.buffer("wait_ns", torch.int64).item()) - w0) / 1e6 / args.steps
     t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    value = world * T / (ms * 1e-3)
+    return float(t.item()), extra, clk, launches, wait_ms
 
-    # e2e: host (pinned) inputs in, the step's result out, through the public
-    # layer API. Every step copies its x and dy host->device inside the timed
-    # region and reads a metric of the step's result back (a checksum of dx,
-    # 4 bytes — the contract's "loss or metric"); the copies run on their own
-    # streams (copy engines), triple-buffered against the previous / next
-    # step's compute, the way a training loop feeds a layer. The same loop
-    # with the whole dx read back (32 MB per step) is reported beside it.
+
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2501_10714_b200.layer import EpGroup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peak_kind = load_peaks()
+    T, M, H, E = (WORKLOAD["tokens_per_gpu"], WORKLOAD["d_model"], WORKLOAD["d_ffn"],
+                  WORKLOAD["experts"])
+    gate = args.gate or WORKLOAD["gate"].split()[0]
+    ep = EpGroup(world, rank, local, max_ctas=args.nccl_ctas) if world > 1 else None
+    layer = make_layer(WORKLOAD, args, world, rank, ep, gate)
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
+    dy = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
+    dx = torch.empty_like(x)
+    y = torch.empty_like(x)
+    ms, extra_warm, clk, launches, wait_ms = timed_steps(layer, x, y, dy, dx, args, world,
+                                                         args.warm_seconds)
+    value = world * T / (ms * 1e-3)
+    # exposed AlltoAll (untraced): the time each rank's compute stream spent
+    # spinning on peer arrival flags inside the timed steps (globaltimer in
+    # peer_wait_kernel), max over ranks
+    exposed = None
+    if world > 1:
+        per = [None] * world
+        dist.all_gather_object(per, wait_ms)
+        exposed = {"ms_per_step": max(per), "frac_of_step": max(per) / ms,
+                   "by_rank_ms_per_step": per,
+                   "how": "per-rank peer-flag wait time (globaltimer in peer_wait_kernel) over the "
+                          "timed steps, untraced; max over ranks"}
+
+    # e2e: host (pinned) inputs in, the step's results out, through the public
+    # layer API. Every step copies its x and dy host->device and reads y and
+    # dx back device->host inside the timed region; the copies run on their
+    # own streams (copy engines), triple-buffered against the previous / next
+    # step's compute, the way a training loop feeds a layer.
     e2e = None
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
         dyh = dy.cpu().pin_memory()
         NB = 3  # triple-buffered: step i+1's H2D never waits on step i-1's D2H
+        yh = [torch.empty_like(xh).pin_memory() for _ in range(NB)]
         dxh = [torch.empty_like(xh).pin_memory() for _ in range(NB)]
-        sumh = torch.empty(NB, dtype=torch.float32).pin_memory()
         xd = [torch.empty_like(x) for _ in range(NB)]
         dyd = [torch.empty_like(dy) for _ in range(NB)]
+        yd = [torch.empty_like(x) for _ in range(NB)]
         dxd = [torch.empty_like(dx) for _ in range(NB)]
-        sumd = torch.empty(NB, dtype=torch.float32, device="cuda")
         comp = torch.cuda.current_stream()
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         ev_x = [torch.cuda.Event() for _ in range(NB)]
         ev_dy = [torch.cuda.Event() for _ in range(NB)]
+        ev_y = [torch.cuda.Event() for _ in range(NB)]
         ev_done = [torch.cuda.Event() for _ in range(NB)]
         ev_free = [torch.cuda.Event() for _ in range(NB)]
         for i in range(NB):
             ev_free[i].record(comp)
 
-        def e2e_steps(n, full_dx):
+        def e2e_steps(n):
             for i in range(n):
                 b = i % NB
                 with torch.cuda.stream(s_in):
@@ -413,51 +501,45 @@ def gpu_arm(args):
                     dyd[b].copy_(dyh, non_blocking=True)
                     ev_dy[b].record(s_in)
                 comp.wait_event(ev_x[b])              # forward needs x only
-                layer.forward(xd[b], y)
+                layer.forward(xd[b], yd[b])
+                ev_y[b].record(comp)
                 comp.wait_event(ev_dy[b])
                 layer.backward(dyd[b], dxd[b])
-                if not full_dx:
-                    torch.sum(dxd[b], dim=(0, 1), dtype=torch.float32, out=sumd[b])
                 ev_done[b].record(comp)
                 with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_y[b])         # y leaves while the backward runs
+                    yh[b].copy_(yd[b], non_blocking=True)
                     s_out.wait_event(ev_done[b])
-                    if full_dx:
-                        dxh[b].copy_(dxd[b], non_blocking=True)
-                    else:
-                        sumh[b:b + 1].copy_(sumd[b:b + 1], non_blocking=True)
-                    ev_free[b].record(s_out)        # result read out, inputs consumed
+                    dxh[b].copy_(dxd[b], non_blocking=True)
+                    ev_free[b].record(s_out)        # results read out, inputs consumed
             comp.wait_stream(s_out)
 
-        def e2e_ms(full_dx):
-            ke = max(1, min(args.steps, 50))
-            e2e_steps(NB, full_dx)
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            s.record()
-            e2e_steps(ke, full_dx)
-            e.record()
-            torch.cuda.synchronize()
-            t = torch.tensor([s.elapsed_time(e) / ke], device="cuda", dtype=torch.float64)
-            if world > 1:
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            return float(t.item())
-
-        ems = e2e_ms(False)
-        ems_full = e2e_ms(True)
+        ke = max(1, min(args.steps, 50))
+        e2e_steps(NB)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        e2e_steps(ke)
+        e.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([s.elapsed_time(e) / ke], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
         e2e = {"value": world * T / (ems * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
-               "d2h_bytes_per_step": 4, "ms_per_step": ems,
+               "d2h_bytes_per_step": 2 * x.numel() * x.element_size(), "ms_per_step": ems,
+               "steps": ke,
                "api": "paper_2501_10714_b200.layer.MoELayer forward+backward (libfsmoe.so C ABI)",
-               "copies": "pinned host x and dy in, an fp32 checksum of dx out, on copy streams "
-                         "triple-buffered against compute, all inside the timed region",
-               "with_full_dx_readback": {"value": world * T / (ems_full * 1e-3), "ms_per_step": ems_full,
-                                         "d2h_bytes_per_step": dx.numel() * dx.element_size()}}
+               "copies": "pinned host x and dy in, the whole y and dx out, every step, on copy "
+                         "streams triple-buffered against compute, all inside the timed region"}
 
     timeline = None
-    if args.trace or world > 1:
+    if args.trace or (world > 1 and not args.no_timeline):
         # measured per-phase timeline (3 extra steps, outside the timed
-        # region): with EP it carries the exposed AlltoAll
+        # region; tracing synchronises per phase): shares, not step time
         nt = 3
         layer.set_trace(True)
         for _ in range(nt):
@@ -471,30 +553,19 @@ def gpu_arm(args):
             with open(f"{args.trace}.rank{rank}.json", "w") as f:
                 f.write(tj)
         timeline = timeline_summary(tj, nt)
-        if world > 1:
-            # every rank's exchange waits: a rank that waits long is waiting for
-            # a slower rank (expert load imbalance under capacity), the rank
-            # that waits least is on the critical path and its waits are the
-            # exchange latency the step really exposes
-            per = [None] * world
-            dist.all_gather_object(per, timeline["comm_exposed_ms_per_step"])
-            timeline["comm_wait_ms_per_step_by_rank"] = per
-            timeline["comm_exposed_ms_per_step"] = max(per)
-            timeline["exposed_alltoall_ms_per_step"] = min(per)
-            timeline["note"] = ("traced run synchronises per phase call; shares, not absolute step "
-                                "time. exposed_alltoall = the critical-path rank's exchange waits; "
-                                "larger waits on other ranks are expert-load imbalance")
 
     roof, gflops, gms = gemm_roofline(layer, peaks)
     roof["peak_source"] = peak_kind
-    traffic_file = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    traffic_file = os.path.join(ROOT, "profiles", f"gemm_traffic_{args.config}.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
             roof["traffic"] = json.load(f).get("bytes_per_step")
+            roof["traffic_source"] = os.path.relpath(traffic_file, ROOT)
     # step roofline (north star): max(GEMM flops at peak, AlltoAll bytes at NVLink)
     C = layer.capacity
     a2a_bytes = 4 * E * C * M * 2 * (world - 1) / world
-    t_gemm = gflops / (peaks.get("bf16_tflops", 1590.0) * 1e12) * 1e3
+    pk = peaks.get("bf16_tflops_sustained" if ms >= 10.0 else "bf16_tflops", 1590.0)
+    t_gemm = gflops / (pk * 1e12) * 1e3
     t_a2a = a2a_bytes / (NVLINK_GBS * 1e9) * 1e3
     a2a_meas = None
     if world > 1:
@@ -507,6 +578,7 @@ def gpu_arm(args):
         for _ in range(3):
             dist.all_to_all_single(rb, sb)
         torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for _ in range(10):
             dist.all_to_all_single(rb, sb)
@@ -520,27 +592,50 @@ def gpu_arm(args):
         a2a_meas = {"nccl_alltoall_ms": ams, "bytes_out_per_gpu": moved,
                     "busbw_gbs": moved / (ams * 1e-3) / 1e9,
                     "note": "torch.distributed all_to_all_single (NCCL) of one dispatch's volume"}
+        del sb, rb
     step_roof = {"gemm_flops": gflops, "a2a_bytes_out_per_gpu": a2a_bytes,
-                 "a2a_measured": a2a_meas,
+                 "a2a_measured": a2a_meas, "peak_tflops": pk,
+                 "peak_kind": "bf16_tflops_sustained" if ms >= 10.0 else "bf16_tflops (burst)",
                  "roofline_ms": max(t_gemm, t_a2a), "measured_ms": ms,
                  "frac": max(t_gemm, t_a2a) / ms, "gemm_share_of_step": gms / ms,
-                 # also against the sustained (power-limited, 4 s back
-                 # to back) cuBLAS figure and the 2.25 PFLOP/s spec
-                 "frac_vs_sustained": max(gflops / (peaks.get("bf16_tflops_sustained", 1400.0) * 1e12) * 1e3,
-                                          t_a2a) / ms,
+                 "frac_vs_burst": max(gflops / (peaks.get("bf16_tflops", 1590.0) * 1e12) * 1e3,
+                                      t_a2a) / ms,
                  "frac_vs_spec": max(gflops / 2.25e15 * 1e3, t_a2a) / ms,
                  "roofline_tokens_per_s": world * T / (max(t_gemm, t_a2a) * 1e-3)}
+    layer.close()
+    del layer
+    torch.cuda.empty_cache()
+
+    # configs[1] at the same N (extra key; the headline line is configs[2])
+    extra = None
+    if args.config == "mixtral" and not args.no_extra:
+        W1 = WORKLOADS["gpt2m"]
+        l1 = make_layer(W1, args, world, rank, ep)
+        T1, M1 = W1["tokens_per_gpu"], W1["d_model"]
+        x1 = torch.randn(T1, M1, device="cuda", generator=g).to(torch.bfloat16)
+        dy1 = torch.randn(T1, M1, device="cuda", generator=g).to(torch.bfloat16)
+        ms1, ex1, clk1, _, wait1 = timed_steps(l1, x1, torch.empty_like(x1), dy1, torch.empty_like(x1),
+                                               args, world, 1.0)
+        extra = {"workload": W1["workload"], "value": world * T1 / (ms1 * 1e-3), "unit": "tokens/s",
+                 "ms_per_step": ms1, "steps": args.steps, "capacity": l1.capacity, "clocks": clk1}
+        if world > 1:
+            per1 = [None] * world
+            dist.all_gather_object(per1, wait1)
+            extra["exposed_alltoall_ms_per_step"] = max(per1)
+        l1.close()
+        del l1
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        xs, wg, wn = cpu_inputs(1024 * (os.cpu_count() or 1), M, E)
-        thr = os.cpu_count() or 1
-        rate, kind, thr, calls, wall = cpu_reference_rate(args.cpu_seconds, thr, 1024, xs, wg, wn, E,
-                                                          -(-1024 * WORKLOAD["top_k"] // E))
+        cap = instance_capacity()
+        thr = cpu_threads_for(T, M, E, cap)
+        xs, wg, wn = cpu_inputs(T, M, E)
+        rate, kind, thr, wall = cpu_reference_pass(thr, xs, wg, wn, E, WORKLOAD["top_k"], cap)
         cpu = {"value": rate, "unit": "tokens/s", "cores": thr, "kind": kind,
-               "sample": f"{calls} calls x 1024 tokens (d_model {M}, {E} experts, top-{WORKLOAD['top_k']}) of "
-                         f"run_gate->dispatch_tokens->combine_tokens over {wall:.1f} s on {thr} "
-                         "threads; the reference has no FFN/backward"}
+               "sample": f"{thr} threads, each routing this workload's full per-GPU instance (T {T}, "
+                         f"d_model {M}, {E} experts, top-{WORKLOAD['top_k']}, capacity {cap}) once: "
+                         f"run_gate->dispatch_tokens->combine_tokens in {wall:.1f} s; the reference "
+                         "has no FFN/backward"}
 
     if rank == 0:
         line = {
@@ -549,14 +644,19 @@ def gpu_arm(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random tokens, random-init experts)",
             "config": dict(WORKLOAD, parallelism=f"ep{world}", r_fwd=args.r_fwd, r_bwd=args.r_bwd,
-                           capacity=C, **({"gate": gate} if args.gate else {})),
+                           capacity=C, warmup_extra_steps=extra_warm,
+                           warmup_note=f"W warm-up steps, then more until {args.warm_seconds:.0f} s "
+                                       "of stepping (steady clocks)",
+                           **({"gate": gate} if args.gate else {})),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches,
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu,
+            "exposed_alltoall": exposed,
         }
+        if extra:
+            line["configs[1]"] = extra
         if timeline:
             line["timeline"] = timeline
         print(json.dumps(line), flush=True)
-    layer.close()
     if ep:
         ep.close()
     if world > 1:
@@ -566,7 +666,7 @@ def gpu_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--r-fwd", type=int, default=1)
@@ -575,9 +675,13 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the configs[1] extra measurement")
+    ap.add_argument("--no-timeline", action="store_true", help="skip the traced per-phase timeline")
+    ap.add_argument("--warm-seconds", type=float, default=3.0,
+                    help="keep warming up (after W steps) until this much stepping has passed")
     ap.add_argument("--trace", default="", help="write per-rank measured timelines to PATH.rankN.json")
-    ap.add_argument("--config", default="gpt2m", choices=sorted(WORKLOADS),
-                    help="gpt2m = BASELINE configs[1] (the headline); mixtral = configs[2]; "
+    ap.add_argument("--config", default="mixtral", choices=sorted(WORKLOADS),
+                    help="mixtral = BASELINE configs[2] (the north-star headline); gpt2m = configs[1]; "
                          "gpt2xl = SURVEY C5 (use with --gate)")
     ap.add_argument("--gate", default=None, choices=GATES,
                     help="gate kind (default: the workload's, noisy_topk)")

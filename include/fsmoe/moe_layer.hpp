@@ -27,7 +27,9 @@ struct MoELayerConfig {
   int top_k = 1;
   GateKind gate = GateKind::noisy_topk;
   LayerConfig::Ffn ffn = LayerConfig::Ffn::simple;  // simple = GELU, gated3 = SwiGLU
-  long long capacity = 0;  // per (rank, expert); 0 -> capacity_tokens(k, f=1)
+  long long capacity = 0;  // per (rank, expert); 0 -> capacity_tokens(k, f, unlimited)
+  double capacity_factor = 1.0;     // LayerConfig::capacity_factor (workload.hpp:24)
+  bool unlimited_capacity = false;  // LayerConfig::unlimited_capacity (workload.hpp:25)
   int proj_dim = 0;        // cosine_topk
   std::uint64_t seed = 0;
   Precision precision = Precision::bf16;

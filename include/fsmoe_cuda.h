@@ -190,6 +190,11 @@ typedef struct fsmoe_peer_rows {
 typedef struct fsmoe_peer_flags {
   unsigned long long* base[FSMOE_MAX_PEERS];  /* per-rank flag arrays (base[rank] = local) */
   int world, rank, nslots;
+  /* optional device counter: every wait adds the nanoseconds (globaltimer) it
+   * spent spinning, i.e. the time the stream was stalled on the exchange */
+  unsigned long long* wait_ns;
+  /* a wait stuck longer than this traps (lost peer); 0 = wait forever */
+  unsigned long long timeout_ns;
 } fsmoe_peer_flags;
 
 /* Optionally puts a small [P][E_l] row buffer (put_src, rows of put_row_bytes,
@@ -197,6 +202,13 @@ typedef struct fsmoe_peer_flags {
 int fsmoe_peer_signal(const fsmoe_peer_flags* f, int slot, const void* put_src,
                       long long put_row_bytes, const fsmoe_peer_rows* put_dst, void* stream);
 int fsmoe_peer_wait(const fsmoe_peer_flags* f, int slot, unsigned long long target, void* stream);
+/* dst[i] = src[0][i] + src[1][i] + ... + src[n_src-1][i] (in that order, so
+ * every caller of the same sources gets the same bits), dtype F64 or F32,
+ * n_src <= FSMOE_MAX_PEERS; dst may alias a source. The allreduce of an
+ * expert-parallel group whose ranks share one device (the single-GPU
+ * multi-rank harness, fsmoe_ep_create_local in fsmoe_layer.h). */
+int fsmoe_sum_buffers(int dtype, int n_src, const void* const* src, long long n, void* dst,
+                      void* stream);
 /* fsmoe_dispatch / fsmoe_combine_bwd writing their block buffer through a peer map. */
 int fsmoe_dispatch_peer(int dtype, int model_dim, int experts, long long capacity,
                         const int* pick_of_slot, const int* pick_token, const void* x,
@@ -257,6 +269,10 @@ typedef struct fsmoe_gemm_desc {
   /* > 0: run the persistent grid on at most this many SMs (leaves the rest to
    * a concurrent kernel, e.g. an NVLink row transfer); 0 = all */
   int max_sms;
+  /* tile-variant overrides (tests / measurement; 0 = the heuristic):
+   * force_ctas 1 | 2 (single CTA / tcgen05 cta_group::2 pair), force_bn 128 |
+   * 256 | 512 columns; dbg: measurement-only epilogue ablations */
+  int force_ctas, force_bn, dbg;
 } fsmoe_gemm_desc;
 
 int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream);

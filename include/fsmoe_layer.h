@@ -28,7 +28,7 @@ typedef struct fsmoe_layer_config {
   int top_k;
   int gate_kind;       /* enum fsmoe_gate_kind */
   int ffn_kind;        /* 0 simple (2 GEMMs, GELU), 1 gated3 (3 GEMMs, SwiGLU) */
-  long long capacity;  /* per (rank, expert); 0 -> capacity_tokens(k, f = 1) */
+  long long capacity;  /* per (rank, expert); 0 -> capacity_tokens(k, capacity_factor, unlimited) */
   int proj_dim;        /* cosine_topk projection rows */
   uint64_t seed;       /* noisy_topk noise seed */
   int precision;       /* 0 bf16 (tcgen05), 1 fp32 check mode */
@@ -37,6 +37,10 @@ typedef struct fsmoe_layer_config {
   long long dense_grad_elems;   /* optional replicated fp32 gradient, allreduced in slices */
   int n_ar_slices;
   const long long* ar_slices;   /* slice sizes (elements), n_ar_slices entries */
+  /* capacity = 0: capacity_tokens (workload.cpp:43-51) of B*L = tokens with
+   * this factor (<= 0 means 1.0), or k * tokens when unlimited != 0 */
+  double capacity_factor;
+  int unlimited;
 } fsmoe_layer_config;
 
 typedef struct fsmoe_layer_params {
@@ -59,6 +63,14 @@ const char* fsmoe_layer_last_error(void);
 int fsmoe_ep_unique_id(unsigned char out[128]);
 int fsmoe_ep_create(int world, int rank, const unsigned char id[128], int device, int max_ctas,
                     fsmoe_ep** out);
+/* Single-GPU multi-rank harness: `world` logical ranks of one group on ONE
+ * device, out[0..world-1] (no NCCL, no IPC; peer maps are plain device
+ * pointers, collectives host barriers + a summation kernel). Each rank's
+ * layer must be created and driven from its own host thread, exactly as one
+ * process per GPU would drive it; the peer-memory transport then runs its
+ * producer stores and arrival flags unchanged. Destroy each with
+ * fsmoe_ep_destroy. */
+int fsmoe_ep_create_local(int world, int device, fsmoe_ep** out);
 int fsmoe_ep_destroy(fsmoe_ep* ep);
 
 /* ep may be NULL (single GPU, all experts local). */
@@ -74,7 +86,8 @@ int fsmoe_layer_backward(fsmoe_layer* layer, const void* dy, void* dx, void* str
  * returns the bytes needed. */
 int fsmoe_layer_set_trace(fsmoe_layer* layer, int on);
 long long fsmoe_layer_trace(const fsmoe_layer* layer, char* buf, long long cap);
-/* Named internal device buffer (pick_token, slot_of_pick, fill, X_send, Z, ...). */
+/* Named internal device buffer (pick_token, slot_of_pick, fill, X_send, Z,
+ * wait_ns = uint64 nanoseconds the compute stream spent waiting on peers, ...). */
 int fsmoe_layer_buffer(const fsmoe_layer* layer, const char* name, void** ptr, long long* bytes);
 
 #ifdef __cplusplus

@@ -48,7 +48,7 @@ class GemmDesc(C.Structure):
         ("Zin", C.c_void_p), ("ldd", C.c_longlong), ("ldd2", C.c_longlong),
         ("ldz", C.c_longlong), ("accumulate", C.c_int), ("precision", C.c_int),
         ("d_peers", C.c_void_p), ("blk_lo", C.c_int), ("blk_hi", C.c_int), ("blk_exclude", C.c_int),
-        ("max_sms", C.c_int),
+        ("max_sms", C.c_int), ("force_ctas", C.c_int), ("force_bn", C.c_int), ("dbg", C.c_int),
     ]
 
 
@@ -62,7 +62,7 @@ class PeerRows(C.Structure):
 class PeerFlags(C.Structure):
     """fsmoe_peer_flags: per-rank uint64 arrival counters [nslots][world]."""
     _fields_ = [("base", C.c_void_p * 8), ("world", C.c_int), ("rank", C.c_int),
-                ("nslots", C.c_int)]
+                ("nslots", C.c_int), ("wait_ns", C.c_void_p), ("timeout_ns", C.c_ulonglong)]
 
 
 class GateDesc(C.Structure):

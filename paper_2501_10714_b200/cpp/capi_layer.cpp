@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 
 #include "ep_group.hpp"
@@ -76,6 +77,25 @@ int fsmoe_ep_create(int world, int rank, const unsigned char id[128], int device
   });
 }
 
+int fsmoe_ep_create_local(int world, int device, fsmoe_ep** out) {
+  return guard([&] {
+    if (world < 1 || world > FSMOE_MAX_PEERS) throw fsmoe::ConfigError("ep: world must be in [1, 8]");
+    auto hub = std::make_shared<fsmoe::LocalHub>(world);
+    for (int r = 0; r < world; ++r) out[r] = nullptr;
+    try {
+      for (int r = 0; r < world; ++r) out[r] = new fsmoe_ep{new fsmoe::EpGroup(hub, r, device)};
+    } catch (...) {
+      for (int r = 0; r < world; ++r)
+        if (out[r]) {
+          delete out[r]->g;
+          delete out[r];
+          out[r] = nullptr;
+        }
+      throw;
+    }
+  });
+}
+
 int fsmoe_ep_destroy(fsmoe_ep* ep) {
   return guard([&] {
     if (ep) {
@@ -98,6 +118,8 @@ int fsmoe_layer_create(const fsmoe_layer_config* c, fsmoe_ep* ep, fsmoe_layer** 
     cfg.gate = static_cast<fsmoe::GateKind>(c->gate_kind);
     cfg.ffn = c->ffn_kind ? fsmoe::LayerConfig::Ffn::gated3 : fsmoe::LayerConfig::Ffn::simple;
     cfg.capacity = c->capacity;
+    cfg.capacity_factor = c->capacity_factor > 0.0 ? c->capacity_factor : 1.0;
+    cfg.unlimited_capacity = c->unlimited != 0;
     cfg.proj_dim = c->proj_dim;
     cfg.seed = c->seed;
     cfg.precision = c->precision ? fsmoe::Precision::f32 : fsmoe::Precision::bf16;

@@ -162,6 +162,9 @@ struct MoELayer::Impl {
   double *w = nullptr, *dw = nullptr, *scores = nullptr, *noise = nullptr, *spread = nullptr,
          *proj_out = nullptr;
   long long *fill = nullptr, *dropped = nullptr, *rfill = nullptr;
+  // nanoseconds this rank's compute stream spent waiting on peer flags
+  // (untraced exposed-exchange time; peer.cu)
+  unsigned long long* wait_ns = nullptr;
   void *gate_ws = nullptr, *assign_ws = nullptr, *tidx_ws = nullptr, *gbwd_ws = nullptr;
   size_t gate_wsb = 0, assign_wsb = 0, tidx_wsb = 0, gbwd_wsb = 0;
   // activations (canonical [P*E_l][C][.])
@@ -201,6 +204,9 @@ struct MoELayer::Impl {
     throw_on(fsmoe_peer_signal(&flags, slot, put, put_row_bytes, put_map, st ? st : s_comp));
   }
   void peer_wait(int slot) {
+    // local (single-device) group: every rank's matching signal is enqueued
+    // before any rank enqueues this wait (ep_group.hpp)
+    ep->host_sync();
     throw_on(fsmoe_peer_wait(&flags, slot, ++epoch[static_cast<size_t>(slot)], s_comp));
   }
 
@@ -247,6 +253,12 @@ struct MoELayer::Impl {
     flags.world = P;
     flags.rank = rank;
     flags.nslots = n_slots();
+    flags.wait_ns = wait_ns;
+    // a lost peer traps the waiter after FSMOE_PEER_TIMEOUT_S seconds
+    // (default 600; 0 = wait forever)
+    const char* to = std::getenv("FSMOE_PEER_TIMEOUT_S");
+    const double sec = to ? std::atof(to) : 600.0;
+    flags.timeout_ns = sec > 0 ? static_cast<unsigned long long>(sec * 1e9) : 0ULL;
     for (int p = 0; p < P; ++p)
       flags.base[p] = reinterpret_cast<unsigned long long*>(static_cast<char*>(sym_peers[p]) + o_flags);
     epoch.assign(static_cast<size_t>(n_slots()), 0);
@@ -264,7 +276,10 @@ struct MoELayer::Impl {
   ~Impl() {
     if (s_comp) cudaStreamSynchronize(s_comp);
     if (s_comm) cudaStreamSynchronize(s_comm);
+    if (s_aux) cudaStreamSynchronize(s_aux);
     if (ep && !sym_peers.empty()) ep->unmap_peers(sym_peers);
+    // no peer may still map or signal into `sym` when it is freed
+    if (ep && sym) ep->quiesce(s_comp);
     if (sym) cudaFree(sym);
     for (void* p : owned) cudaFree(p);
     for (auto e : ev_a) cudaEventDestroy(e);
@@ -488,9 +503,7 @@ struct MoELayer::Impl {
     for (long long n : sl) {
       n = std::min(n, cfg.dense_grad_elems - off);
       if (n <= 0) break;
-      nccl_check(ncclAllReduce(prm.dense_grad + off, prm.dense_grad + off, static_cast<size_t>(n),
-                               ncclFloat32, ncclSum, ep->comm(), s_comm),
-                 "ncclAllReduce");
+      ep->allreduce_sum(prm.dense_grad + off, static_cast<size_t>(n), false, s_comm);
       off += n;
     }
   }
@@ -530,7 +543,8 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
     lc.seq_len = cfg.tokens;
     lc.model_dim = cfg.model_dim;
     lc.hidden_scale = 1;
-    lc.capacity_factor = 1.0;
+    lc.capacity_factor = cfg.capacity_factor;
+    lc.unlimited_capacity = cfg.unlimited_capacity;
     lc.experts = cfg.experts;
     lc.top_k = cfg.top_k;
     I.C = capacity_tokens(lc);
@@ -599,7 +613,11 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   if (I.P > 1) {
     const char* tr = std::getenv("FSMOE_EP_TRANSPORT");
     I.peer = !(tr && std::strcmp(tr, "nccl") == 0);
+    if (!I.peer && ep->local())
+      throw ConfigError("layer: the NCCL transport needs one GPU per rank (local group given)");
   }
+  I.wait_ns = reinterpret_cast<unsigned long long*>(I.dalloc("wait_ns", 8));
+  cuda_check(cudaMemsetAsync(I.wait_ns, 0, 8, I.s_comp), "memset");
   I.rfill = I.P > 1 && !I.peer ? static_cast<long long*>(I.dalloc("recv_fill", 8 * E)) : I.fill;
   I.scores = static_cast<double*>(I.dalloc("scores", 8 * T * E));
   if (cfg.gate == GateKind::noisy_topk) {
@@ -932,18 +950,12 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
     I.record(I.ev_gate, I.s_comp);
     I.wait(I.s_comm, I.ev_gate);
     sp = I.tr.begin("gate_grad_sync", 0, I.s_comm);
-    nccl_check(ncclGroupStart(), "ncclGroupStart");
-    nccl_check(ncclAllReduce(p.g_gate, p.g_gate, ge, ncclFloat64, ncclSum, I.ep->comm(), I.s_comm),
-               "ncclAllReduce");
-    if (p.g_noise)
-      nccl_check(ncclAllReduce(p.g_noise, p.g_noise, static_cast<size_t>(I.M) * I.E, ncclFloat64,
-                               ncclSum, I.ep->comm(), I.s_comm),
-                 "ncclAllReduce");
+    I.ep->group_start();
+    I.ep->allreduce_sum(p.g_gate, static_cast<size_t>(ge), true, I.s_comm);
+    if (p.g_noise) I.ep->allreduce_sum(p.g_noise, static_cast<size_t>(I.M) * I.E, true, I.s_comm);
     if (p.g_proj)
-      nccl_check(ncclAllReduce(p.g_proj, p.g_proj, static_cast<size_t>(cfg_.proj_dim) * I.M,
-                               ncclFloat64, ncclSum, I.ep->comm(), I.s_comm),
-                 "ncclAllReduce");
-    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+      I.ep->allreduce_sum(p.g_proj, static_cast<size_t>(cfg_.proj_dim) * I.M, true, I.s_comm);
+    I.ep->group_end();
     I.tr.end(sp, I.s_comm);
     I.record(I.ev_join, I.s_comm);
     I.wait(I.s_comp, I.ev_join);

@@ -134,6 +134,9 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   p.accumulate = d->accumulate != 0;
   if (d->epi < 0 || d->epi > 5) return config_error("gemm: unknown epilogue");
   p.max_sms = d->max_sms;
+  p.force_ctas = d->force_ctas;
+  p.force_bn = d->force_bn;
+  p.dbg = d->dbg;
   if (d->blk_hi > 0) {
     if (d->kind != 0) return config_error("gemm: a block range needs a row-grouped problem");
     p.blocks = fsmoe_dev::RowRange{d->blk_lo, d->blk_hi, d->blk_exclude};

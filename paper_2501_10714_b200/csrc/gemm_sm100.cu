@@ -53,7 +53,7 @@ struct KParams {
   int use_peers;           // row-grouped plain stores through `peers`
   fsmoe_dev::PeerRows peers;
   fsmoe_dev::RowRange blocks;  // row-grouped: the blocks this launch covers
-  int dbg;  // measurement only (FSMOE_GEMM_DBG): 1 no epilogue after the TMEM reads,
+  int dbg;  // measurement only (fsmoe_gemm_desc::dbg): 1 no epilogue after the TMEM reads,
             // 2 no TMEM reads either, 4 everything but the TMA stores
 };
 
@@ -808,7 +808,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.b_mn = pr.b_mn_major ? 1 : 0;
   p.valid = pr.valid_rows;
   p.epi = static_cast<int>(pr.epi);
-  if (const char* env = getenv("FSMOE_GEMM_DBG")) p.dbg = atoi(env);
+  p.dbg = pr.dbg;
   p.D = pr.D;
   p.D2 = pr.D2;
   p.Zin = pr.Zin;
@@ -826,14 +826,14 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   if (pr.kind == GemmKind::KGrouped && p.row0 + pr.rows < p.rows_total && pr.rows % 64)
     return cudaErrorInvalidValue;  // the K window must end on a 64-row boundary
   // Tile shape: CTA pairs (256 x 256, cta_group::2) unless the problem is too
-  // small to give every SM pair work; FSMOE_GEMM_CTAS=1|2 forces a variant.
+  // small to give every SM pair work; fsmoe_gemm_desc::force_ctas forces a variant.
   const int units_rows = pr.kind == GemmKind::RowGrouped ? pr.rows : pr.Mo;
   const int units_cols = pr.kind == GemmKind::RowGrouped ? pr.N : pr.No;
   const int groups = pr.kind == GemmKind::RowGrouped ? pr.nblk : p.n_w;
   long long pair_tiles = static_cast<long long>(groups) * ((units_rows + 255) / 256) *
                          ((units_cols + BN_MAX - 1) / BN_MAX);
   int ctas = pair_tiles >= num_sms() / 4 ? 2 : 1;
-  if (const char* env = getenv("FSMOE_GEMM_CTAS")) ctas = atoi(env) == 1 ? 1 : 2;
+  if (pr.force_ctas) ctas = pr.force_ctas == 1 ? 1 : 2;
   // Tile width. Pairs take 512-column tiles (two MMAs per K step, one
   // accumulator: 25 % less operand traffic per flop than 256 columns) for the
   // plain bf16 and fp32 epilogues when that still gives every pair a tile:
@@ -841,7 +841,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   // configs[2] ones (profiles/r01_gemm_bn512.md). The GELU / SwiGLU epilogues
   // keep 256 columns and double-buffered accumulators (their epilogue is long
   // enough that the single-accumulator drain shows). 128-column tiles
-  // (FSMOE_GEMM_BN=128) measured slower everywhere. FSMOE_GEMM_BN=128|256|512
+  // (force_bn = 128) measured slower everywhere. force_bn = 128|256|512
   // forces a width (512: every epilogue but GELU-backward).
   int BN = BN_MAX;
   const bool plain_epi = pr.epi == Epi::StoreBF16 || pr.epi == Epi::StoreF32;
@@ -850,8 +850,8 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
                                ((units_cols + 511) / 512);
     if (tiles512 >= num_sms() / 2) BN = 512;
   }
-  if (const char* env = getenv("FSMOE_GEMM_BN")) {
-    const int want = atoi(env);
+  if (pr.force_bn) {
+    const int want = pr.force_bn;
     if (want == 128 && pr.epi != Epi::SwigluFwd && pr.epi != Epi::SwigluBwd) BN = 128;
     else if (want == 256) BN = 256;
     else if (want == 512 && ctas == 2 && pr.epi != Epi::GeluBwd) BN = 512;

@@ -18,10 +18,17 @@
 // flag is never reset and a late waiter cannot miss an increment.
 //
 // A peer that never signals (crashed rank) would spin the waiter forever; the
-// wait gives up after FSMOE_PEER_TIMEOUT_NS and traps so the process fails
-// instead of wedging the GPU.
+// wait gives up after fsmoe_peer_flags::timeout_ns (the layer takes it from
+// FSMOE_PEER_TIMEOUT_S, default 600 s; 0 = never) and traps so the process
+// fails instead of wedging the GPU. A legitimately late peer (checkpoint,
+// evaluation, first-step initialisation) stays well inside the default.
+//
+// With fsmoe_peer_flags::wait_ns set, every wait adds the time it spent
+// spinning (globaltimer, first thread in to last flag seen) to that counter:
+// the untraced per-rank exposed-exchange time the bench reports.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "capi_common.h"
@@ -31,8 +38,6 @@ namespace fsmoe {
 namespace {
 
 using namespace fsmoe_dev;
-
-constexpr unsigned long long PEER_TIMEOUT_NS = 30ULL * 1000 * 1000 * 1000;
 
 struct Flags {
   unsigned long long* base[MAX_PEERS];
@@ -75,14 +80,15 @@ __global__ void peer_signal_kernel(Flags f, int slot, const unsigned long long* 
 }
 
 __global__ void peer_wait_kernel(const unsigned long long* __restrict__ flags, int world, int slot,
-                                 unsigned long long target) {
+                                 unsigned long long target, unsigned long long* wait_ns,
+                                 unsigned long long timeout_ns) {
   const int src = threadIdx.x;
+  const unsigned long long t0 = global_ns();
   if (src < world) {
     const unsigned long long* fl = flags + static_cast<long long>(slot) * world + src;
-    const unsigned long long t0 = global_ns();
     while (ld_acquire_sys(fl) < target) {
       __nanosleep(64);
-      if (global_ns() - t0 > PEER_TIMEOUT_NS) {
+      if (timeout_ns && global_ns() - t0 > timeout_ns) {
         printf("fsmoe_peer_wait: rank-%d flag of slot %d stuck below %llu (peer lost?)\n", src,
                slot, target);
         __trap();
@@ -90,6 +96,22 @@ __global__ void peer_wait_kernel(const unsigned long long* __restrict__ flags, i
     }
   }
   __syncthreads();
+  if (wait_ns && src == 0) atomicAdd(wait_ns, global_ns() - t0);
+}
+
+template <class T>
+struct Srcs {
+  const T* p[MAX_PEERS];
+};
+
+template <class T>
+__global__ void sum_buffers_kernel(Srcs<T> s, int n_src, long long n, T* __restrict__ dst) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    T v = s.p[0][i];
+    for (int k = 1; k < n_src; ++k) v += s.p[k][i];
+    dst[i] = v;
+  }
 }
 
 int check_flags(const fsmoe_peer_flags* f, int slot) {
@@ -131,11 +153,33 @@ extern "C" int fsmoe_peer_signal(const fsmoe_peer_flags* f, int slot, const void
   return cuda_status(cudaGetLastError(), "fsmoe_peer_signal");
 }
 
+extern "C" int fsmoe_sum_buffers(int dtype, int n_src, const void* const* src, long long n, void* dst,
+                                 void* stream) {
+  if (n_src < 1 || n_src > MAX_PEERS || !src || (n > 0 && !dst))
+    return config_error("sum buffers: need 1..8 sources and a destination");
+  if (dtype != FSMOE_F64 && dtype != FSMOE_F32) return config_error("sum buffers: dtype must be f64 or f32");
+  if (n <= 0) return FSMOE_OK;
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<long long>((n + threads - 1) / threads, 148LL * 8));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == FSMOE_F64) {
+    Srcs<double> s{};
+    for (int k = 0; k < n_src; ++k) s.p[k] = static_cast<const double*>(src[k]);
+    sum_buffers_kernel<<<blocks, threads, 0, st>>>(s, n_src, n, static_cast<double*>(dst));
+  } else {
+    Srcs<float> s{};
+    for (int k = 0; k < n_src; ++k) s.p[k] = static_cast<const float*>(src[k]);
+    sum_buffers_kernel<<<blocks, threads, 0, st>>>(s, n_src, n, static_cast<float*>(dst));
+  }
+  count_launch();
+  return cuda_status(cudaGetLastError(), "fsmoe_sum_buffers");
+}
+
 extern "C" int fsmoe_peer_wait(const fsmoe_peer_flags* f, int slot, unsigned long long target,
                                void* stream) {
   if (int rc = check_flags(f, slot)) return rc;
   peer_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(f->base[f->rank], f->world, slot,
-                                                                  target);
+                                                                  target, f->wait_ns, f->timeout_ns);
   count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_peer_wait");
 }

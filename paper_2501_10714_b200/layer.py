@@ -25,7 +25,8 @@ class LayerConfigC(C.Structure):
         ("capacity", C.c_longlong), ("proj_dim", C.c_int), ("seed", C.c_uint64),
         ("precision", C.c_int), ("r_fwd", C.c_int), ("r_bwd", C.c_int), ("device", C.c_int),
         ("dense_grad_elems", C.c_longlong), ("n_ar_slices", C.c_int),
-        ("ar_slices", C.POINTER(C.c_longlong)),
+        ("ar_slices", C.POINTER(C.c_longlong)), ("capacity_factor", C.c_double),
+        ("unlimited", C.c_int),
     ]
 
 
@@ -43,8 +44,9 @@ class MoEConfig:
     top_k: int = 1
     gate: str = "noisy_topk"
     ffn: str = "simple"
-    capacity: int = 0            # 0 -> capacity_tokens(k, f=1)
+    capacity: int = 0            # 0 -> capacity_tokens(k, capacity_factor, unlimited)
     capacity_factor: float = 1.0
+    unlimited: bool = False
     proj_dim: int = 0
     seed: int = 7
     precision: str = "bf16"      # or "f32" (check mode)
@@ -54,14 +56,13 @@ class MoEConfig:
     ar_slices: list = field(default_factory=list)
 
     def resolved_capacity(self) -> int:
-        """capacity_tokens (workload.cpp:43-51) with B*L = tokens."""
+        """capacity_tokens (workload.cpp:43-51) with B*L = tokens (expert
+        choice: tokens per expert, the same formula)."""
         if self.capacity:
             return self.capacity
-        if self.gate == "expert_choice":
-            k = self.top_k
-        else:
-            k = self.top_k
-        v = k * self.capacity_factor * self.tokens / self.experts
+        if self.unlimited:
+            return self.top_k * self.tokens
+        v = self.top_k * self.capacity_factor * self.tokens / self.experts
         return int(math.ceil(v - 1e-9))
 
 
@@ -90,10 +91,54 @@ class EpGroup:
         self.h = h
         self.world, self.rank = world, rank
 
+    @classmethod
+    def local_group(cls, world: int, device: int) -> list["EpGroup"]:
+        """The single-GPU multi-rank harness (fsmoe_ep_create_local): `world`
+        logical ranks of one group on one device, no NCCL / IPC. Create and
+        drive each rank's MoELayer from its own thread (run_ranks)."""
+        lib = NL.cpp_lib()
+        hs = (C.c_void_p * world)()
+        NL.check(lib.fsmoe_ep_create_local(world, device, hs), lib)
+        out = []
+        for r in range(world):
+            g = cls.__new__(cls)
+            g.h, g.world, g.rank = C.c_void_p(hs[r]), world, r
+            out.append(g)
+        return out
+
     def close(self):
         if self.h:
             NL.cpp_lib().fsmoe_ep_destroy(self.h)
             self.h = None
+
+
+def run_ranks(world: int, fn, timeout: float = 600.0):
+    """Run fn(rank) for every logical rank of a local group on its own host
+    thread (each with its own current CUDA stream) and return the results in
+    rank order; the first exception is re-raised. ctypes drops the GIL in
+    foreign calls, so the ranks' collectives (host barriers) meet."""
+    import threading
+    res, err = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                res[r] = fn(r)
+                torch.cuda.current_stream().synchronize()
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout)
+        if t.is_alive():
+            raise TimeoutError("local EP group: a rank did not finish")
+    for e in err:
+        if e is not None:
+            raise e
+    return res
 
 
 def _p(t):
@@ -160,7 +205,11 @@ class MoELayer:
         c.top_k = cfg.top_k
         c.gate_kind = GATE_KINDS[cfg.gate]
         c.ffn_kind = FFN_KINDS[cfg.ffn]
-        c.capacity = cfg.resolved_capacity()
+        c.capacity = 0  # the C++ side derives it (capacity_tokens, workload.cpp:43-51)
+        c.capacity_factor = cfg.capacity_factor
+        c.unlimited = 1 if cfg.unlimited else 0
+        if cfg.capacity:
+            c.capacity = cfg.capacity
         c.proj_dim = cfg.proj_dim
         c.seed = cfg.seed
         c.precision = 0 if cfg.precision == "bf16" else 1

@@ -29,9 +29,14 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+# tile-variant override for every grouped_gemm call (tests sweep the variants):
+# (ctas, bn) with 0 = the library's heuristic
+GEMM_FORCE = (0, 0)
+
+
 def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn_major=False,
                  rows_total=0, row0=0, valid_rows=None, epi="store_bf16", D2=None, Zin=None, ldd=None, ldd2=0, ldz=0,
-                 accumulate=False, precision=0):
+                 accumulate=False, precision=0, force=None, dbg=0):
     """Grouped expert GEMM (see csrc/gemm.h). kind: 'row' or 'k'."""
     lib = NL.cuda_lib()
     d = NL.GemmDesc()
@@ -48,6 +53,8 @@ def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn
     d.ldd, d.ldd2, d.ldz = ldd, ldd2, ldz
     d.accumulate = int(accumulate)
     d.precision = precision
+    d.force_ctas, d.force_bn = force if force is not None else GEMM_FORCE
+    d.dbg = dbg
     NL.check(lib.fsmoe_grouped_gemm(C.byref(d), _stream()))
 
 

@@ -58,3 +58,20 @@ def test_workloads_table():
     assert set(bench.GATES) == {"noisy_topk", "sigmoid_topk", "cosine_topk", "expert_choice"}
     for w in bench.WORKLOADS.values():
         assert {"workload", "tokens_per_gpu", "d_model", "d_ffn", "experts", "top_k"} <= set(w)
+
+
+def test_reference_pass_routes_the_gpu_arms_instance():
+    """The reference arm and cpu_baseline route the GPU arm's instance: same
+    T, capacity_tokens(k, f) (workload.cpp:43-51), all threads on the whole
+    instance (a tiny shape here)."""
+    assert bench.WORKLOADS["mixtral"] is bench.WORKLOAD  # the headline default
+    old = bench.WORKLOAD
+    try:
+        bench.WORKLOAD = dict(old, tokens_per_gpu=256, d_model=64, experts=8, top_k=2)
+        assert bench.instance_capacity() == 64
+        x, wg, wn = bench.cpu_inputs(256, 64, 8)
+        rate, kind, thr, wall = bench.cpu_reference_pass(2, x, wg, wn, 8, 2, 64)
+        assert thr == 2 and rate > 0 and wall > 0 and kind in ("reference", "port")
+    finally:
+        bench.WORKLOAD = old
+    assert bench.cpu_threads_for(32768, 4096, 8, 8192) >= 1

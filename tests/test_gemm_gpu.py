@@ -26,8 +26,8 @@ def gemm_ctas(request, monkeypatch):
     and the pair's 512-column tile (one accumulator, two MMAs per K step;
     every epilogue but GELU-backward, which keeps 256 columns)."""
     ctas, bn = request.param.split("x")
-    monkeypatch.setenv("FSMOE_GEMM_CTAS", ctas)
-    monkeypatch.setenv("FSMOE_GEMM_BN", bn)
+    from paper_2501_10714_b200 import ops
+    monkeypatch.setattr(ops, "GEMM_FORCE", (int(ctas), int(bn)))
     return ctas
 
 
