@@ -90,6 +90,14 @@ int fsmoe_gate(const fsmoe_gate_desc* d, const void* x, const double* w_score,
                double* noise_out, double* spread_out, double* proj_out,
                int* d_status, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Parity audit of the gate's libm (no reference counterpart): y = f(x) on
+ * the device for fn 0 log, 1 exp, 2 log1p, 3 cos, 4 the normal draw
+ * sqrt(-2 log x) cos(2 pi x2) (workload.cpp:90-95), 5 softplus
+ * log1p(exp(x)) (101); impl 0 = the glibc 2.39 restatement the gate runs
+ * (bit-identical to the host libm the reference calls), 1 = CUDA's libm. */
+int fsmoe_libm_eval(int fn, int impl, const double* x, const double* x2, double* y, long long n,
+                    void* stream);
+
 /* Synchronises `stream`, reads the device status word written by gate /
  * assign and converts it to the reference's ConfigError (return 2 + message). */
 int fsmoe_check_status(const int* d_status, void* stream);

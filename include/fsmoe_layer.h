@@ -72,6 +72,11 @@ int fsmoe_ep_create(int world, int rank, const unsigned char id[128], int device
  * fsmoe_ep_destroy. */
 int fsmoe_ep_create_local(int world, int device, fsmoe_ep** out);
 int fsmoe_ep_destroy(fsmoe_ep* ep);
+/* In-place sum of n fp32 (f64 = 0) or fp64 (f64 = 1) elements over the
+ * group, stream-ordered on `stream` (NCCL allreduce; local group: barrier +
+ * in-order summation, same bits on every rank). The tail of the gradient
+ * partition plan (grad_partition.hpp) runs through it. */
+int fsmoe_ep_allreduce(fsmoe_ep* ep, void* buf, long long n, int f64, void* stream);
 
 /* ep may be NULL (single GPU, all experts local). */
 int fsmoe_layer_create(const fsmoe_layer_config* cfg, fsmoe_ep* ep, fsmoe_layer** out);

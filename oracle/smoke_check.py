@@ -1,4 +1,6 @@
-"""One small MoE-layer forward + backward on cuda:0 through the product path
+"""TEST INFRASTRUCTURE ONLY — the body of __graft_entry__.smoke().
+
+One small MoE-layer forward + backward on cuda:0 through the product path
 (libfsmoe.so C++ layer -> libfsmoe_cuda.so sm_100a kernels), routing checked
 pick-by-pick against the CPU oracle (test infrastructure) and outputs /
 gradients against the fp64 restatement."""
@@ -10,17 +12,18 @@ import sys
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # repo root
 
 
 def run() -> None:
     if not torch.cuda.is_available():
         raise RuntimeError("smoke() needs a CUDA device (there is no CPU fallback)")
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, ROOT)
     import layer_oracle  # test infrastructure (checker only)
     import pyoracle
 
-    from .layer import MoEConfig, MoELayer
+    from paper_2501_10714_b200.layer import MoEConfig, MoELayer
 
     torch.cuda.set_device(0)
     T, M, H, E, k = 512, 256, 512, 8, 2

@@ -96,6 +96,15 @@ int fsmoe_ep_create_local(int world, int device, fsmoe_ep** out) {
   });
 }
 
+int fsmoe_ep_allreduce(fsmoe_ep* ep, void* buf, long long n, int f64, void* stream) {
+  return guard([&] {
+    if (!ep || (n > 0 && !buf)) throw fsmoe::ConfigError("ep allreduce: null group or buffer");
+    if (n <= 0) return;
+    fsmoe::throw_cuda(cudaSetDevice(ep->g->device()), "cudaSetDevice");
+    ep->g->allreduce_sum(buf, static_cast<size_t>(n), f64 != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int fsmoe_ep_destroy(fsmoe_ep* ep) {
   return guard([&] {
     if (ep) {

@@ -28,6 +28,7 @@
 
 #include "capi_common.h"
 #include "host_once.h"
+#include "glibc_libm.cuh"
 #include "kernels.h"
 #include "route_common.cuh"
 
@@ -260,7 +261,7 @@ __device__ __forceinline__ double box_muller(uint64_t a, uint64_t b) {
   double u1 = __dmul_rn(__dadd_rn(static_cast<double>(a >> 11), 0.5), 0x1.0p-53);
   double u2 = __dmul_rn(__dadd_rn(static_cast<double>(b >> 11), 0.5), 0x1.0p-53);
   double two_pi = 2.0 * 3.141592653589793238462643383279502884;
-  return __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
+  return fsmoe_libm::gl_normal(u1, u2);
 }
 
 // ------------------------------------------------------- token selection --
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(128)
     mt64_outputs<2 * MAX_E>(seed + static_cast<uint64_t>(t), 2 * E, draws);
     for (int e = 0; e < E; ++e) {
       double n = box_muller(draws[2 * e], draws[2 * e + 1]);
-      double sp = log1p(exp(spread[static_cast<long long>(t) * E + e]));
+      double sp = fsmoe_libm::gl_softplus(spread[static_cast<long long>(t) * E + e]);
       s[e] = __dadd_rn(raw[static_cast<long long>(t) * E + e], __dmul_rn(n, sp));
       if (noise_out) noise_out[static_cast<long long>(t) * E + e] = n;
     }
@@ -331,18 +332,18 @@ __global__ void __launch_bounds__(128)
     for (int j = 0; j < k; ++j) {
       pick_token[base + j] = t;
       pick_expert[base + j] = keep[j];
-      pick_weight[base + j] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-s[keep[j]])));
+      pick_weight[base + j] = __ddiv_rn(1.0, __dadd_rn(1.0, fsmoe_libm::gl_exp(-s[keep[j]])));
     }
     return;
   }
   double mx = s[keep[0]];
   for (int j = 0; j < k; ++j) mx = (mx < s[keep[j]]) ? s[keep[j]] : mx;
   double z = 0.0;
-  for (int j = 0; j < k; ++j) z = __dadd_rn(z, exp(__dsub_rn(s[keep[j]], mx)));
+  for (int j = 0; j < k; ++j) z = __dadd_rn(z, fsmoe_libm::gl_exp(__dsub_rn(s[keep[j]], mx)));
   for (int j = 0; j < k; ++j) {
     pick_token[base + j] = t;
     pick_expert[base + j] = keep[j];
-    pick_weight[base + j] = __ddiv_rn(exp(__dsub_rn(s[keep[j]], mx)), z);
+    pick_weight[base + j] = __ddiv_rn(fsmoe_libm::gl_exp(__dsub_rn(s[keep[j]], mx)), z);
   }
 }
 
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(EC_THREADS)
   for (int i = 1; i < EC_THREADS / 32; ++i) mx = s_red[i] > mx ? s_red[i] : mx;
   double* wts = pick_weight + static_cast<long long>(e) * C;
   __syncthreads();
-  for (int j = threadIdx.x; j < C; j += EC_THREADS) wts[j] = exp(__dsub_rn(wts[j], mx));
+  for (int j = threadIdx.x; j < C; j += EC_THREADS) wts[j] = fsmoe_libm::gl_exp(__dsub_rn(wts[j], mx));
   __threadfence_block();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -611,3 +612,52 @@ size_t gate_workspace_bytes(const fsmoe_gate_desc& d) {
 }
 
 }  // namespace fsmoe
+
+// ------------------------------------------------------------ libm audit --
+// fsmoe_libm_eval: the gate's transcendental functions on the device, either
+// the glibc restatement the gate uses (impl 0, glibc_libm.cuh) or CUDA's own
+// libm (impl 1), for the parity audit against the host's glibc
+// (tests/test_noise_exact_gpu.py).
+namespace {
+__global__ void libm_eval_kernel(int fn, int impl, const double* __restrict__ x,
+                                 const double* __restrict__ x2, double* __restrict__ y, long long n) {
+  using namespace fsmoe_libm;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double a = x[i];
+    double r = 0.0;
+    if (impl == 0) {
+      switch (fn) {
+        case 0: r = gl_log(a); break;
+        case 1: r = gl_exp(a); break;
+        case 2: r = gl_log1p(a); break;
+        case 3: r = gl_cos(a); break;
+        case 4: r = gl_normal(a, x2[i]); break;
+        default: r = gl_softplus(a); break;
+      }
+    } else {
+      const double two_pi = 2.0 * 3.141592653589793238462643383279502884;
+      switch (fn) {
+        case 0: r = log(a); break;
+        case 1: r = exp(a); break;
+        case 2: r = log1p(a); break;
+        case 3: r = cos(a); break;
+        case 4: r = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(a))), cos(__dmul_rn(two_pi, x2[i]))); break;
+        default: r = log1p(exp(a)); break;
+      }
+    }
+    y[i] = r;
+  }
+}
+}  // namespace
+
+extern "C" int fsmoe_libm_eval(int fn, int impl, const double* x, const double* x2, double* y,
+                               long long n, void* stream) {
+  if (fn < 0 || fn > 5 || impl < 0 || impl > 1 || (n > 0 && (!x || !y)) || (fn == 4 && n > 0 && !x2))
+    return fsmoe::config_error("libm eval: fn in [0, 5], impl 0 | 1, x and y required (x2 for fn 4)");
+  if (n <= 0) return FSMOE_OK;
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
+  libm_eval_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(fn, impl, x, x2, y, n);
+  fsmoe::count_launch();
+  return fsmoe::cuda_status(cudaGetLastError(), "fsmoe_libm_eval");
+}

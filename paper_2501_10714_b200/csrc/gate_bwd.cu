@@ -133,14 +133,7 @@ constexpr int XT_TCH = 256;  // tokens per partial (at most; fewer when that lea
 // that chunks x column blocks gives the GPU two blocks per SM (small T, or a
 // narrow M such as the cosine projection's P rows).
 inline int xt_tch(int T, long long colblocks) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  const long long want = 2LL * sms;
+  const long long want = 2LL * device_sms();
   const long long nch = (want + colblocks - 1) / colblocks;
   long long tch = (T + nch - 1) / nch;
   tch = (tch + 31) / 32 * 32;

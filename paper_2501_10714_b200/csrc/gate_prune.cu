@@ -37,6 +37,7 @@
 
 #include "host_once.h"
 #include "capi_common.h"
+#include "glibc_libm.cuh"
 #include "kernels.h"
 #include "route_common.cuh"
 #include "sm100.cuh"
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(256)
     double u1 = __dmul_rn(__dadd_rn(static_cast<double>(o0 >> 11), 0.5), 0x1.0p-53);
     double u2 = __dmul_rn(__dadd_rn(static_cast<double>(o1 >> 11), 0.5), 0x1.0p-53);
     double two_pi = 2.0 * 3.141592653589793238462643383279502884;
-    const double n = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
+    const double n = fsmoe_libm::gl_normal(u1, u2);
     const double bs = cB * xnorm * wn[E + e];
     const double soft = log1p(exp(static_cast<double>(sp)));
     s = static_cast<double>(r) + n * soft;
@@ -439,10 +440,8 @@ void launch_exact(const void* x, int T, int M, int E, const PruneWsView& w, cuda
                       (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   if (staged) {
     constexpr int SMEM = 2 * (EX_TOK * Elem<DT>::ROW + NPROJ * Elem<DT>::JC * 8);
-    static std::atomic<unsigned> attr{0};
-    if (first_on_device(attr)) {
-      cudaFuncSetAttribute(exact_staged_kernel<DT, NPROJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    }
+    static DeviceOnce attr;
+    once_on_device(attr, [&] { cudaFuncSetAttribute(exact_staged_kernel<DT, NPROJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM); });
     dim3 g((T + EX_TOK - 1) / EX_TOK, E);
     exact_staged_kernel<DT, NPROJ><<<g, EX_TOK * NPROJ, SMEM, st>>>(x, T, M, E, w.WT, w.lists, w.counts,
                                                                  w.s_exact, w.sp_exact);
@@ -473,7 +472,7 @@ __global__ void __launch_bounds__(128)
     if (KIND == 0)  // s = raw + n * softplus(spread)   (workload.cpp:186)
       for (uint64_t m = cand; m; m &= m - 1) {
         const long long o = row + __ffsll(static_cast<long long>(m)) - 1;
-        s_exact[o] = __dadd_rn(s_exact[o], __dmul_rn(noise[o], log1p(exp(sp_exact[o]))));
+        s_exact[o] = __dadd_rn(s_exact[o], __dmul_rn(noise[o], fsmoe_libm::gl_softplus(sp_exact[o])));
       }
     uint64_t kept = 0;
     for (int j = 0; j < k; ++j) {
@@ -497,7 +496,7 @@ __global__ void __launch_bounds__(128)
         m &= m - 1;
         pick_token[base + j] = t;
         pick_expert[base + j] = e;
-        pick_weight[base + j] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-s_exact[row + e])));
+        pick_weight[base + j] = __ddiv_rn(1.0, __dadd_rn(1.0, fsmoe_libm::gl_exp(-s_exact[row + e])));
       }
     } else {
       uint64_t m = kept;
@@ -508,14 +507,14 @@ __global__ void __launch_bounds__(128)
       }
       double z = 0.0;
       for (m = kept; m; m &= m - 1)
-        z = __dadd_rn(z, exp(__dsub_rn(s_exact[row + __ffsll(static_cast<long long>(m)) - 1], mx)));
+        z = __dadd_rn(z, fsmoe_libm::gl_exp(__dsub_rn(s_exact[row + __ffsll(static_cast<long long>(m)) - 1], mx)));
       m = kept;
       for (int j = 0; j < k; ++j) {
         const int e = __ffsll(static_cast<long long>(m)) - 1;
         m &= m - 1;
         pick_token[base + j] = t;
         pick_expert[base + j] = e;
-        pick_weight[base + j] = __ddiv_rn(exp(__dsub_rn(s_exact[row + e], mx)), z);
+        pick_weight[base + j] = __ddiv_rn(fsmoe_libm::gl_exp(__dsub_rn(s_exact[row + e], mx)), z);
       }
     }
   }
@@ -787,7 +786,7 @@ __global__ void __launch_bounds__(512 + SC_MT_WARPS * 32)
       const double u1 = __dmul_rn(__dadd_rn(static_cast<double>(o0 >> 11), 0.5), 0x1.0p-53);
       const double u2 = __dmul_rn(__dadd_rn(static_cast<double>(o1 >> 11), 0.5), 0x1.0p-53);
       const double two_pi = 2.0 * 3.141592653589793238462643383279502884;
-      const double n = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
+      const double n = fsmoe_libm::gl_normal(u1, u2);
       const double bs = cB * xnorm * wn[E + e];
       const double soft = log1p(exp(static_cast<double>(sp)));
       s = static_cast<double>(r) + n * soft;
@@ -959,7 +958,7 @@ __global__ void __launch_bounds__(XF_THREADS)
           const double d0 = rd[(tid * E_MAX + e) * 2], d1 = rd[(tid * E_MAX + e) * 2 + 1];
           const double a0 = ra[(tid * E_MAX + e) * 2], a1 = ra[(tid * E_MAX + e) * 2 + 1];
           const double n = noise[static_cast<long long>(t0 + tl) * E + e];
-          const double soft = log1p(exp(d1));
+          const double soft = fsmoe_libm::gl_softplus(d1);
           const double sv = d0 + n * soft;
           const double b = g * (a0 + fabs(n) * a1) +
                            8.0 * u * (fabs(d0) + fabs(n * soft) + fabs(n) * soft) + 1e-300;
@@ -1114,7 +1113,7 @@ __global__ void __launch_bounds__(XF_THREADS)
   for (uint64_t m = cand; m; m &= m - 1) {
     const int e = __ffsll(static_cast<long long>(m)) - 1;
     if (KIND == 0) {  // s = raw + n * softplus(spread)   (workload.cpp:186)
-      s[e] = __dadd_rn(s[e], __dmul_rn(noise[row + e], log1p(exp(ex[NPROJ - 1][tid][e]))));
+      s[e] = __dadd_rn(s[e], __dmul_rn(noise[row + e], fsmoe_libm::gl_softplus(ex[NPROJ - 1][tid][e])));
       if (spread_out) spread_out[row + e] = ex[NPROJ - 1][tid][e];
     }
     if (scores_out) scores_out[row + e] = s[e];
@@ -1140,7 +1139,7 @@ __global__ void __launch_bounds__(XF_THREADS)
       m &= m - 1;
       pick_token[pb + j] = t;
       pick_expert[pb + j] = e;
-      pick_weight[pb + j] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-s[e])));
+      pick_weight[pb + j] = __ddiv_rn(1.0, __dadd_rn(1.0, fsmoe_libm::gl_exp(-s[e])));
     }
   } else {
     uint64_t m = kept;
@@ -1150,14 +1149,14 @@ __global__ void __launch_bounds__(XF_THREADS)
       mx = (mx < v) ? v : mx;
     }
     double z = 0.0;
-    for (m = kept; m; m &= m - 1) z = __dadd_rn(z, exp(__dsub_rn(s[__ffsll(static_cast<long long>(m)) - 1], mx)));
+    for (m = kept; m; m &= m - 1) z = __dadd_rn(z, fsmoe_libm::gl_exp(__dsub_rn(s[__ffsll(static_cast<long long>(m)) - 1], mx)));
     m = kept;
     for (int j = 0; j < k; ++j) {
       const int e = __ffsll(static_cast<long long>(m)) - 1;
       m &= m - 1;
       pick_token[pb + j] = t;
       pick_expert[pb + j] = e;
-      pick_weight[pb + j] = __ddiv_rn(exp(__dsub_rn(s[e], mx)), z);
+      pick_weight[pb + j] = __ddiv_rn(fsmoe_libm::gl_exp(__dsub_rn(s[e], mx)), z);
     }
   }
 }
@@ -1172,19 +1171,15 @@ void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const floa
   const double u = 0x1.0p-24;
   const double gam = M * u / (1.0 - M * u);
   constexpr int SMEM = ScreenSmem<NCP, E_MAX>::BYTES;
-  static std::atomic<unsigned> attr{0};
-  if (first_on_device(attr)) {
-    cudaFuncSetAttribute(screen_kernel<KIND, NCP, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  }
+  static DeviceOnce attr;
+  once_on_device(attr, [&] { cudaFuncSetAttribute(screen_kernel<KIND, NCP, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM); });
   const auto* xb = static_cast<const __nv_bfloat16*>(x);
   screen_kernel<KIND, NCP, E_MAX><<<(T + SC_TOK - 1) / SC_TOK, 512 + SC_MT_WARPS * 32, SMEM, st>>>(
       xb, T, M, E, k, W32, NC, wn, cB, gam, d.seed, noise_ws, scores_out, spread_out, mask);
   ::fsmoe::count_launch();
   constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
-  static std::atomic<unsigned> xattr{0};
-  if (first_on_device(xattr)) {
-    cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM);
-  }
+  static DeviceOnce xattr;
+  once_on_device(xattr, [&] { cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM); });
   exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, XSMEM, st>>>(
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
       spread_out);

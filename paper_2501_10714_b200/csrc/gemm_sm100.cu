@@ -782,14 +782,7 @@ bool make_map3s(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_
 }
 
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+  return device_sms();
 }
 
 }  // namespace
@@ -922,10 +915,10 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   const int sms = pr.max_sms > 0 && pr.max_sms < num_sms() ? pr.max_sms : num_sms();
   const int max_units = sms / ctas > 0 ? sms / ctas : 1;
   const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
-  static std::atomic<unsigned> smem_set[2][3];
+  static DeviceOnce smem_set[2][3];
   auto launch = [&](auto kern, int smem) -> cudaError_t {
-    if (first_on_device(smem_set[ctas - 1][BN == 128 ? 0 : BN == 256 ? 1 : 2]))
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    once_on_device(smem_set[ctas - 1][BN == 128 ? 0 : BN == 256 ? 1 : 2],
+                   [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(units * ctas);
     cfg.blockDim = dim3(NUM_THREADS);

@@ -1,33 +1,53 @@
-// host_once.h — per-device one-time host setup (kernel attributes).
+// host_once.h — per-device one-time host setup (kernel attributes) and cached
+// device properties, safe for a process that drives several GPUs from
+// several threads.
 #pragma once
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 
 namespace fsmoe {
 
-// True the first time it is called for the current device with this flag:
-// cudaFuncSetAttribute is per device, so a process driving several GPUs must
-// set it on each.
-inline bool first_on_device(std::atomic<unsigned>& seen) {
+constexpr int kMaxDevices = 32;
+
+inline int current_device() {
   int d = 0;
   cudaGetDevice(&d);
-  const unsigned bit = 1u << (d & 31);
-  return (seen.fetch_or(bit) & bit) == 0;
+  return d & (kMaxDevices - 1);
+}
+
+// One std::once_flag per device: cudaFuncSetAttribute is per device, and a
+// second thread on the same device must not launch before the first one's
+// attribute call has returned (call_once blocks it until then).
+struct DeviceOnce {
+  std::once_flag flag[kMaxDevices];
+};
+
+template <class F>
+void once_on_device(DeviceOnce& o, F&& fn) {
+  std::call_once(o.flag[current_device()], fn);
+}
+
+// SM count of the current device (cached per device).
+inline int device_sms() {
+  static std::atomic<int> sms[kMaxDevices];
+  const int d = current_device();
+  int v = sms[d].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    sms[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
 }
 
 // Threads per block for thread-per-token kernels: 128, or 32 when 128 would
 // put the work on fewer than two blocks per SM (small token counts: spread
 // the latency-bound per-token loops over every SM).
 inline int per_token_block(long long T) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return (T + 127) / 128 >= 2LL * sms ? 128 : 32;
+  return (T + 127) / 128 >= 2LL * device_sms() ? 128 : 32;
 }
 
 }  // namespace fsmoe

@@ -332,21 +332,27 @@ __global__ void __launch_bounds__(32)
 
 // persistent grid for the bulk row movers: every resident block slot, at
 // most one block per group
+// (occupancy cached per kernel, device and shared-memory size)
 template <typename K>
 int bulk_grid(K kern, int smem, long long ngroups) {
-  static int cached_smem = -1, per_sm = 1;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static std::mutex mu;
+  static int cached_smem[kMaxDevices], cached_per_sm[kMaxDevices];
+  static bool valid[kMaxDevices];
+  const int dev = current_device();
+  int per_sm = 1;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (valid[dev] && cached_smem[dev] == smem) {
+      per_sm = cached_per_sm[dev];
+    } else {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+      cached_smem[dev] = smem;
+      cached_per_sm[dev] = per_sm;
+      valid[dev] = true;
+    }
   }
-  if (smem != cached_smem) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem) != cudaSuccess || per_sm < 1)
-      per_sm = 1;
-    cached_smem = smem;
-  }
-  const long long slots = static_cast<long long>(per_sm) * sms;
+  const long long slots = static_cast<long long>(per_sm) * device_sms();
   return static_cast<int>(ngroups < slots ? ngroups : slots);
 }
 
@@ -706,10 +712,8 @@ int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, co
   if (n_rows <= 0) return FSMOE_OK;
   if (row_bytes % 16 != 0 || row_bytes > 4096)
     return config_error("gather_rows: row bytes must be a multiple of 16 and at most 4096");
-  static std::atomic<unsigned> attr{0};
-  if (first_on_device(attr)) {
-    cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
-  }
+  static DeviceOnce attr;
+  once_on_device(attr, [&] { cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096); });
   const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
   gather_bulk_kernel<<<bulk_grid(gather_bulk_kernel, smem, (n_rows + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
       n_rows, static_cast<int>(row_bytes), idx, static_cast<const uint8_t*>(src), dst);
@@ -726,10 +730,8 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
   const int grid = static_cast<int>((n_slots + 7) / 8);
   if (row_bytes % 16 == 0 && row_bytes <= 4096 && !getenv("FSMOE_ROUTE_NOBULK")) {
     const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
-    static std::atomic<unsigned> attr{0};
-    if (first_on_device(attr)) {
-      cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096);
-    }
+    static DeviceOnce attr;
+    once_on_device(attr, [&] { cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096); });
     dispatch_bulk_kernel<<<bulk_grid(dispatch_bulk_kernel, smem, (n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
         n_slots, static_cast<int>(row_bytes), E, C, chunks, pick_of_slot, ptok,
         static_cast<const uint8_t*>(x), buf, rr);

@@ -106,6 +106,16 @@ class EpGroup:
             out.append(g)
         return out
 
+    def allreduce(self, t: torch.Tensor):
+        """In-place sum of an fp32 / fp64 CUDA tensor over the group, on the
+        current stream (fsmoe_ep_allreduce)."""
+        assert t.is_cuda and t.is_contiguous() and t.dtype in (torch.float32, torch.float64)
+        lib = NL.cpp_lib()
+        NL.check(lib.fsmoe_ep_allreduce(self.h, C.c_void_p(t.data_ptr()), C.c_longlong(t.numel()),
+                                        1 if t.dtype == torch.float64 else 0,
+                                        C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)), lib)
+        return t
+
     def close(self):
         if self.h:
             NL.cpp_lib().fsmoe_ep_destroy(self.h)

@@ -109,8 +109,8 @@ class MoEStack:
             if produce is not None:
                 produce(j, self.pool[j * self.n_grad: (j + 1) * self.n_grad])
         if self.world > 1 and ptr < self.pool.numel():
-            import torch.distributed as dist
-            dist.all_reduce(self.pool[ptr:])
+            # the tail, over the layers' own EP communicator (libfsmoe.so)
+            self.ep.allreduce(self.pool[ptr:])
         return dy
 
     def close(self):
