@@ -217,6 +217,17 @@ int fsmoe_peer_wait(const fsmoe_peer_flags* f, int slot, unsigned long long targ
  * multi-rank harness, fsmoe_ep_create_local in fsmoe_layer.h). */
 int fsmoe_sum_buffers(int dtype, int n_src, const void* const* src, long long n, void* dst,
                       void* stream);
+/* Copy-engine exchange of one pipeline chunk (no SM work): for every rank p
+ * (p == rank only with include_self), rows [lo, hi) of the E_l blocks
+ * destined to p in the local canonical send buffer (block b = p*E_l + e_l,
+ * `capacity` rows each, dst->capacity) are copied into p's receive map at
+ * [rank][e_l][lo, hi). fsmoe_peer_flag_write then sets flag[slot][rank] to
+ * `value` on every rank behind the stream's earlier work (stream memory
+ * operation with a system-scope fence; `value` = how many times this rank
+ * has signalled the slot, matching fsmoe_peer_wait's counting). */
+int fsmoe_peer_copy_rows(const void* send, long long row_bytes, const fsmoe_peer_rows* dst, long long lo,
+                         long long hi, int include_self, void* stream);
+int fsmoe_peer_flag_write(const fsmoe_peer_flags* f, int slot, unsigned long long value, void* stream);
 /* fsmoe_dispatch / fsmoe_combine_bwd writing their block buffer through a peer map. */
 int fsmoe_dispatch_peer(int dtype, int model_dim, int experts, long long capacity,
                         const int* pick_of_slot, const int* pick_token, const void* x,

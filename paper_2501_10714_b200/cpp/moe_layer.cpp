@@ -192,12 +192,41 @@ struct MoELayer::Impl {
   std::vector<unsigned long long> epoch;
   bool last_was_bwd = false;
   int slot_bar_fwd() const { return 0; }
-  int slot_disp_fwd() const { return 1; }
-  int slot_comb_fwd(size_t j) const { return 2 + static_cast<int>(j); }
-  int slot_disp_bwd() const { return 2 + n_chunk_slots; }
-  int slot_comb_bwd(size_t j) const { return 3 + n_chunk_slots + static_cast<int>(j); }
-  int slot_bar_bwd() const { return 3 + 2 * n_chunk_slots; }
-  int n_slots() const { return 4 + 2 * n_chunk_slots; }
+  int slot_disp_fwd(size_t j) const { return 1 + static_cast<int>(j); }
+  int slot_comb_fwd(size_t j) const { return 1 + n_chunk_slots + static_cast<int>(j); }
+  int slot_disp_bwd(size_t j) const { return 1 + 2 * n_chunk_slots + static_cast<int>(j); }
+  int slot_comb_bwd(size_t j) const { return 1 + 3 * n_chunk_slots + static_cast<int>(j); }
+  int slot_bar_bwd() const { return 1 + 4 * n_chunk_slots; }
+  int n_slots() const { return 2 + 4 * n_chunk_slots; }
+  // Copy-engine transport (FSMOE_EP_TRANSPORT=ce): FSMoE's chunked pipeline
+  // for the dispatch-side exchanges. The permutation kernels write this
+  // rank's own rows straight into its receive buffer and the peers' rows into
+  // a canonical send buffer (stage maps); the copy engines move pipeline
+  // chunk i to every peer on s_ce while the expert GEMMs of chunk i-1 hold
+  // the SMs, and a stream memory write raises chunk i's flag behind them.
+  // The combine-side exchanges stay fused into the GEMM epilogues.
+  bool ce = false;
+  cudaStream_t s_ce = nullptr;
+  cudaEvent_t ev_ce = nullptr;
+  void *Xsend = nullptr, *dOsend = nullptr;
+  fsmoe_peer_rows stage_X{}, stage_dO{};
+  std::vector<unsigned long long> sig_count;
+  void ce_signal(int slot) {
+    throw_on(fsmoe_peer_flag_write(&flags, slot, ++sig_count[static_cast<size_t>(slot)], s_ce));
+  }
+  // rows of block b = p*E_l + e_l: own (p == rank) into the receive buffer,
+  // the peers' into the canonical send buffer at [p E_l + e_l][C]
+  fsmoe_peer_rows stage_map(void* recv_local, void* send) const {
+    fsmoe_peer_rows m{};
+    m.world = P;
+    m.rank = rank;
+    m.experts_local = El;
+    m.capacity = C;
+    const long long blk = static_cast<long long>(El) * C * M * esz;
+    for (int p = 0; p < P; ++p)
+      m.base[p] = p == rank ? recv_local : static_cast<char*>(send) + (p - rank) * blk;
+    return m;
+  }
 
   void peer_signal(int slot, const void* put = nullptr, long long put_row_bytes = 0,
                    const fsmoe_peer_rows* put_map = nullptr, cudaStream_t st = nullptr) {
@@ -277,6 +306,7 @@ struct MoELayer::Impl {
     if (s_comp) cudaStreamSynchronize(s_comp);
     if (s_comm) cudaStreamSynchronize(s_comm);
     if (s_aux) cudaStreamSynchronize(s_aux);
+    if (s_ce) cudaStreamSynchronize(s_ce);
     if (ep && !sym_peers.empty()) ep->unmap_peers(sym_peers);
     // no peer may still map or signal into `sym` when it is freed
     if (ep && sym) ep->quiesce(s_comp);
@@ -292,6 +322,8 @@ struct MoELayer::Impl {
     }
     if (s_comp) cudaStreamDestroy(s_comp);
     if (s_comm) cudaStreamDestroy(s_comm);
+    if (s_ce) cudaStreamDestroy(s_ce);
+    if (ev_ce) cudaEventDestroy(ev_ce);
   }
 
   // ------------------------------------------------------------- GEMMs --
@@ -613,6 +645,7 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   if (I.P > 1) {
     const char* tr = std::getenv("FSMOE_EP_TRANSPORT");
     I.peer = !(tr && std::strcmp(tr, "nccl") == 0);
+    I.ce = tr && std::strcmp(tr, "ce") == 0;
     if (!I.peer && ep->local())
       throw ConfigError("layer: the NCCL transport needs one GPU per rank (local group given)");
   }
@@ -638,10 +671,20 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   const long long ab = rows * M * I.esz;
   if (I.peer) {
     const char* sp_env = std::getenv("FSMOE_EP_SPLIT");
-    I.split = I.fwd_chunks.size() == 1 && I.bwd_chunks.size() == 1 && sp_env && std::atoi(sp_env) > 0;
+    I.split = !I.ce && I.fwd_chunks.size() == 1 && I.bwd_chunks.size() == 1 && sp_env &&
+              std::atoi(sp_env) > 0;
     if (I.split) I.split_sms = std::atoi(sp_env) > 1 ? std::atoi(sp_env) : 0;
     I.n_chunk_slots = static_cast<int>(std::max(I.fwd_chunks.size(), I.bwd_chunks.size()));
     I.setup_peer(ab);
+    if (I.ce) {
+      I.Xsend = I.dalloc("X_send", ab);
+      I.dOsend = I.dalloc("dO_send", ab);
+      I.stage_X = I.stage_map(I.Xr, I.Xsend);
+      I.stage_dO = I.stage_map(I.dOr, I.dOsend);
+      I.sig_count.assign(static_cast<size_t>(I.n_slots()), 0);
+      cuda_check(cudaStreamCreateWithPriority(&I.s_ce, cudaStreamNonBlocking, hi), "stream");
+      cuda_check(cudaEventCreateWithFlags(&I.ev_ce, cudaEventDisableTiming), "event");
+    }
     I.Z = I.dalloc("Z", rows * I.N1 * I.esz);
     I.Hh = I.dalloc("H", rows * I.H * I.esz);
     cuda_check(cudaMemsetAsync(I.status, 0, 8, I.s_comp), "memset");
@@ -722,13 +765,13 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
     I.wait(I.s_aux, I.ev_x1);
     throw_on(fsmoe_dispatch_peer_range(I.dtype, I.M, I.E, I.C, I.pos, I.tok, x, &I.map_X, lo, hi, 1,
                                        I.s_aux));
-    I.peer_signal(I.slot_disp_fwd(), I.fill, 8, &I.map_fill, I.s_aux);
+    I.peer_signal(I.slot_disp_fwd(0), I.fill, 8, &I.map_fill, I.s_aux);
     I.record(I.ev_x2, I.s_aux);
     sp = I.tr.begin("expert-local", 2, I.s_comp);
     I.expert_fwd(ch[0], 1);
     I.tr.end(sp, I.s_comp);
     sp = I.tr.begin("dispatch", 0, I.s_comp);
-    I.peer_wait(I.slot_disp_fwd());
+    I.peer_wait(I.slot_disp_fwd(0));
     I.wait(I.s_comp, I.ev_x2);
     I.tr.end(sp, I.s_comp);
     sp = I.tr.begin("expert[0]", 2, I.s_comp);
@@ -738,13 +781,40 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
     sp = I.tr.begin("combine", 0, I.s_comp);
     I.peer_wait(I.slot_comb_fwd(0));
     I.tr.end(sp, I.s_comp);
+  } else if (I.peer && I.ce) {
+    // the permutation keeps own rows local and stages the peers' rows; the
+    // copy engines ship chunk i while GEMM chunk i-1 runs
+    sp = I.tr.begin("order-stage", 2, I.s_comp);
+    I.peer_wait(I.slot_bar_fwd());
+    throw_on(fsmoe_dispatch_peer(I.dtype, I.M, I.E, I.C, I.pos, I.tok, x, &I.stage_X, I.s_comp));
+    I.tr.end(sp, I.s_comp);
+    I.record(I.ev_ce, I.s_comp);
+    I.wait(I.s_ce, I.ev_ce);
+    throw_on(fsmoe_peer_copy_rows(I.fill, 8, &I.map_fill, 0, 1, 1, I.s_ce));
+    for (size_t i = 0; i < ch.size(); ++i) {
+      throw_on(fsmoe_peer_copy_rows(I.Xsend, static_cast<long long>(I.M) * I.esz, &I.map_X, ch[i].lo,
+                                    ch[i].hi, 0, I.s_ce));
+      I.ce_signal(I.slot_disp_fwd(i));
+    }
+    for (size_t i = 0; i < ch.size(); ++i) {
+      sp = I.tr.begin("dispatch[" + std::to_string(i) + "]", 0, I.s_comp);
+      I.peer_wait(I.slot_disp_fwd(i));
+      I.tr.end(sp, I.s_comp);
+      sp = I.tr.begin("expert[" + std::to_string(i) + "]", 2, I.s_comp);
+      I.expert_fwd(ch[i]);
+      I.peer_signal(I.slot_comb_fwd(i));
+      I.tr.end(sp, I.s_comp);
+    }
+    sp = I.tr.begin("combine", 0, I.s_comp);
+    for (size_t i = 0; i < ch.size(); ++i) I.peer_wait(I.slot_comb_fwd(i));
+    I.tr.end(sp, I.s_comp);
   } else if (I.peer) {
     // order + dispatch AlltoAll in one kernel: rows go straight to their owner
     sp = I.tr.begin("dispatch", 0, I.s_comp);
     I.peer_wait(I.slot_bar_fwd());
     throw_on(fsmoe_dispatch_peer(I.dtype, I.M, I.E, I.C, I.pos, I.tok, x, &I.map_X, I.s_comp));
-    I.peer_signal(I.slot_disp_fwd(), I.fill, 8, &I.map_fill);
-    I.peer_wait(I.slot_disp_fwd());
+    I.peer_signal(I.slot_disp_fwd(0), I.fill, 8, &I.map_fill);
+    I.peer_wait(I.slot_disp_fwd(0));
     I.tr.end(sp, I.s_comp);
     for (size_t i = 0; i < ch.size(); ++i) {
       // GEMM2's epilogue stores the combine AlltoAll into the owners' O_send
@@ -825,7 +895,24 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
     }
     // I-order backward fused with the dispatch AlltoAll of dO
     const bool split_bwd = I.split && cfg_.precision == Precision::bf16;
-    if (split_bwd) {
+    if (I.ce) {
+      // I-order backward: own dO rows local, the peers' staged; the copy
+      // engines ship chunk j while the expert backward of chunk j-1 runs
+      sp = I.tr.begin("i-order", 2, I.s_comp);
+      if (I.unit_top1)
+        throw_on(fsmoe_dispatch_peer(I.dtype, I.M, I.E, I.C, I.pos, I.tok, dy, &I.stage_dO, I.s_comp));
+      else
+        throw_on(fsmoe_combine_bwd_peer(I.dtype, I.M, I.E, I.C, I.n_picks, I.pos, I.tok, I.w, dy, I.Os,
+                                        &I.stage_dO, I.dw, I.s_comp));
+      I.tr.end(sp, I.s_comp);
+      I.record(I.ev_ce, I.s_comp);
+      I.wait(I.s_ce, I.ev_ce);
+      for (size_t j = 0; j < ch.size(); ++j) {
+        throw_on(fsmoe_peer_copy_rows(I.dOsend, static_cast<long long>(I.M) * I.esz, &I.map_dO, ch[j].lo,
+                                      ch[j].hi, 0, I.s_ce));
+        I.ce_signal(I.slot_disp_bwd(j));
+      }
+    } else if (split_bwd) {
       // own experts' dO rows first, the peers' rows on s_aux over NVLink while
       // dgrad2 already runs on the local blocks
       const long long lo = static_cast<long long>(I.rank) * I.El * I.C, hi = lo + I.El * I.C;
@@ -845,13 +932,13 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
       I.record(I.ev_x1, I.s_comp);
       I.wait(I.s_aux, I.ev_x1);
       iorder(1, I.s_aux);
-      I.peer_signal(I.slot_disp_bwd(), nullptr, 0, nullptr, I.s_aux);
+      I.peer_signal(I.slot_disp_bwd(0), nullptr, 0, nullptr, I.s_aux);
       I.record(I.ev_x2, I.s_aux);
       sp = I.tr.begin("expert-local", 2, I.s_comp);
       I.expert_bwd(ch[0], true, 1);
       I.tr.end(sp, I.s_comp);
       sp = I.tr.begin("dispatch", 0, I.s_comp);
-      I.peer_wait(I.slot_disp_bwd());
+      I.peer_wait(I.slot_disp_bwd(0));
       I.wait(I.s_comp, I.ev_x2);
       I.tr.end(sp, I.s_comp);
     } else {
@@ -863,8 +950,8 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
                                         I.Os, &I.map_dO, I.dw, I.s_comp));
       I.tr.end(sp, I.s_comp);
       sp = I.tr.begin("dispatch", 0, I.s_comp);
-      I.peer_signal(I.slot_disp_bwd());
-      I.peer_wait(I.slot_disp_bwd());
+      I.peer_signal(I.slot_disp_bwd(0));
+      I.peer_wait(I.slot_disp_bwd(0));
       I.tr.end(sp, I.s_comp);
     }
     if (I.prm.dense_grad && cfg_.dense_grad_elems > 0) {
@@ -877,6 +964,11 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
       I.record(I.ev_join, I.s_comm);
     }
     for (size_t j = 0; j < ch.size(); ++j) {
+      if (I.ce) {
+        sp = I.tr.begin("dispatch[" + std::to_string(j) + "]", 0, I.s_comp);
+        I.peer_wait(I.slot_disp_bwd(j));
+        I.tr.end(sp, I.s_comp);
+      }
       // dgrad1's epilogue stores the combine AlltoAll into the owners' dX_send
       sp = I.tr.begin("expert[" + std::to_string(j) + "]", 2, I.s_comp);
       I.expert_bwd(ch[j], j == 0, split_bwd ? 2 : 0);

@@ -479,6 +479,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         c2 = p.peers.rank * p.peers.el + (ti.g - pp * p.peers.el);
         md = &em.peer[pp];
       }
+      if (p.epi == static_cast<int>(Epi::SwigluBwd)) {
+        // prefetch this warp's first saved gate / up box pair while the MMAs run
+        const int col = ti.nt * BN + CPH * half * 32;
+        if (lane == 0 && col < p.out_cols) {
+          const int gcol = (col / 128) * 256 + (col % 128);
+          bulk_wait_read<0>();  // the previous tile's stores have left the boxes
+          mbar_arrive_expect_tx(&zb[0], 4096);
+          tma_load_3d(stg, &em.z, &zb[0], gcol, c1, ti.g);
+          mbar_arrive_expect_tx(&zb[1], 4096);
+          tma_load_3d(stg + 4096, &em.z, &zb[1], gcol + 128, c1, ti.g);
+        }
+        __syncwarp();
+      }
       if (p.epi == static_cast<int>(Epi::GeluBwd)) {
         // prefetch this warp's saved gelu'(Z) boxes while the MMAs still run
         if (lane == 0) {
@@ -648,72 +661,149 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // every 256 tile columns: [0,128) gate units, [128,256) up units (the
         // same 128 units). A 256-column tile splits its 128 units over the two
         // warp halves; a 512-column tile gives each half one 256-column block.
+        // Per 64 units (two 32-column TMEM chunks): the bf16 gate and up
+        // pre-activations go out as two 32-row x 128-byte TMA boxes (Z), then
+        // H = silu(gate) * up (from the bf16-rounded values the backward
+        // sees) as a third box through the first buffer once its store read.
         constexpr int NSUB = BN >= 256 ? BN / 256 : 1;
         const int sub = NSUB == 2 ? half : 0;
         const int c_lo = NSUB == 2 ? 0 : 2 * half;
         const int c_hi = c_lo + (NSUB == 2 ? 4 : 2);
         const uint32_t tsub = tbase + sub * 256;
-        __nv_bfloat16* Z = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-        __nv_bfloat16* H = static_cast<__nv_bfloat16*>(p.D2) + orow * p.ldd2;
-        for (int c = c_lo; c < c_hi; ++c) {
-          float g[32];
-          if (nkb > 0) {
-            tmem_ld_32x32b_x32(tsub + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) g[i] = __uint_as_float(r[i]);
-            tmem_ld_32x32b_x32(tsub + 128 + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) g[i] = v[i] = 0.f;
-          }
+        uint4* bz0 = box_row(stg);
+        uint4* bz1 = box_row(stg + 4096);
+        for (int c = c_lo; c < c_hi; c += 2) {
           const int gcol = ti.nt * BN + sub * 256 + c * 32;
           const int hcol = ti.nt * (BN / 2) + sub * 128 + c * 32;
-          if (row_ok && gcol < p.out_cols) {
-            store_bf16x32(Z + gcol, g);
-            store_bf16x32(Z + gcol + 128, v);
-            float h[32];
+          if (lane == 0) bulk_wait_read<0>();  // both buffers free
+          __syncwarp();
+          uint32_t gp[32];  // bf16 pairs: gate of the two chunks
+          uint32_t hp[32];  // bf16 pairs: H of the two chunks
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float gb = bf2f(__float2bfloat16(g[i]));
-              float ub = bf2f(__float2bfloat16(v[i]));
-              h[i] = gb * sigmoid_f(gb) * ub;
+          for (int j = 0; j < 2; ++j) {
+            if (nkb > 0) {
+              tmem_ld_32x32b_x32(tsub + (c + j) * 32, r);
+              tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = 0u;
             }
-            store_bf16x32(H + hcol, h);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+              gp[16 * j + i] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              bz0[(4 * j + k) ^ sw] = make_uint4(gp[16 * j + 4 * k], gp[16 * j + 4 * k + 1],
+                                                 gp[16 * j + 4 * k + 2], gp[16 * j + 4 * k + 3]);
+            if (nkb > 0) {
+              tmem_ld_32x32b_x32(tsub + 128 + (c + j) * 32, r);
+              tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = 0u;
+            }
+            if (j == 1 && c + 2 >= c_hi) release_acc();
+            uint32_t up[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              __nv_bfloat162 u2 = __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+              up[i] = *reinterpret_cast<uint32_t*>(&u2);
+              const float2 gb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gp[16 * j + i]));
+              const float2 ub = __bfloat1622float2(u2);
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(gb.x * sigmoid_f(gb.x) * ub.x,
+                                                        gb.y * sigmoid_f(gb.y) * ub.y);
+              hp[16 * j + i] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              bz1[(4 * j + k) ^ sw] = make_uint4(up[4 * k], up[4 * k + 1], up[4 * k + 2], up[4 * k + 3]);
+          }
+          if (gcol >= p.out_cols) continue;  // warp-uniform (after the TMEM reads)
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            store_box(md, stg, gcol, c1, c2);
+            store_box(md, stg + 4096, gcol + 128, c1, c2);
+            bulk_commit();
+            bulk_wait_read<0>();
+          }
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            bz0[k ^ sw] = make_uint4(hp[4 * k], hp[4 * k + 1], hp[4 * k + 2], hp[4 * k + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            store_box(&em.d2, stg, hcol, c1, c2);
+            bulk_commit();
           }
         }
       } else {  // SwigluBwd: acc = dH over H units; dZ at the interleaved gate/up columns
-        const __nv_bfloat16* Z = static_cast<const __nv_bfloat16*>(p.Zin) + orow * p.ldz;
-        __nv_bfloat16* dZ = static_cast<__nv_bfloat16*>(p.D) + orow * p.ldd;
-        for (int c = CPH * half; c < CPH * half + CPH; ++c) {
+        // Per 64 units: the saved bf16 gate / up boxes come in by TMA (the
+        // first pair was prefetched while the MMAs ran), dG / dU are written
+        // over them and go back out to the same place (dZ over Z).
+        for (int pc = 0; pc < CPH / 2; ++pc) {
+          const int c = CPH * half + 2 * pc;
           const int col = ti.nt * BN + c * 32;
+          const int gcol = (col / 128) * 256 + (col % 128);
+          uint32_t r2[32];
           if (nkb > 0) {
             tmem_ld_32x32b_x32(tbase + c * 32, r);
+            tmem_ld_32x32b_x32(tbase + (c + 1) * 32, r2);
             tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            for (int i = 0; i < 32; ++i) r[i] = r2[i] = 0u;
           }
-          if (!row_ok || col >= p.out_cols) continue;
-          const int gcol = (col / 128) * 256 + (col % 128);
-          float g[32], u[32];
-          load_bf16x32(Z + gcol, g);
-          load_bf16x32(Z + gcol + 128, u);
+          if (pc == CPH / 2 - 1) release_acc();
+          if (col >= p.out_cols) continue;  // warp-uniform
+          if (pc > 0) {  // this pair was not prefetched: load it now
+            if (lane == 0) {
+              bulk_wait_read<0>();
+              mbar_arrive_expect_tx(&zb[0], 4096);
+              tma_load_3d(stg, &em.z, &zb[0], gcol, c1, ti.g);
+              mbar_arrive_expect_tx(&zb[1], 4096);
+              tma_load_3d(stg + 4096, &em.z, &zb[1], gcol + 128, c1, ti.g);
+            }
+            __syncwarp();
+          }
+          mbar_wait(&zb[0], zph[0]);
+          zph[0] ^= 1u;
+          mbar_wait(&zb[1], zph[1]);
+          zph[1] ^= 1u;
+          uint4* bg = box_row(stg);
+          uint4* bu = box_row(stg + 4096);
+          auto dv = [&](int i) { return __uint_as_float(i < 32 ? r[i] : r2[i - 32]); };
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float sg = sigmoid_f(g[i]);
-            const float silu = g[i] * sg;
-            const float dg = v[i] * u[i] * sg * (1.0f + g[i] * (1.0f - sg));
-            u[i] = v[i] * silu;
-            g[i] = dg;
+          for (int k = 0; k < 8; ++k) {
+            uint4 gw = bg[k ^ sw], uw = bu[k ^ sw];
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gw);
+            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uw);
+            uint32_t og[4], ou[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 g = __bfloat1622float2(g2[j]);
+              const float2 u = __bfloat1622float2(u2[j]);
+              const float d0 = dv(8 * k + 2 * j), d1 = dv(8 * k + 2 * j + 1);
+              const float s0 = sigmoid_f(g.x), s1 = sigmoid_f(g.y);
+              __nv_bfloat162 dg = __floats2bfloat162_rn(d0 * u.x * s0 * (1.0f + g.x * (1.0f - s0)),
+                                                        d1 * u.y * s1 * (1.0f + g.y * (1.0f - s1)));
+              __nv_bfloat162 du = __floats2bfloat162_rn(d0 * (g.x * s0), d1 * (g.y * s1));
+              og[j] = *reinterpret_cast<uint32_t*>(&dg);
+              ou[j] = *reinterpret_cast<uint32_t*>(&du);
+            }
+            bg[k ^ sw] = make_uint4(og[0], og[1], og[2], og[3]);
+            bu[k ^ sw] = make_uint4(ou[0], ou[1], ou[2], ou[3]);
           }
-          store_bf16x32(dZ + gcol, g);
-          store_bf16x32(dZ + gcol + 128, u);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            store_box(md, stg, gcol, c1, c2);
+            store_box(md, stg + 4096, gcol + 128, c1, c2);
+            bulk_commit();
+          }
         }
       }
       if (!released) release_acc();
@@ -883,6 +973,23 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     const bool f32 = pr.epi == Epi::StoreF32;
     const uint64_t es = f32 ? 4 : 2;
     const uint32_t bc = f32 ? 32 : 64;
+    if (pr.epi == Epi::SwigluFwd || pr.epi == Epi::SwigluBwd) {
+      // Z (2N interleaved gate / up columns, or N of them for the forward's
+      // N = 2H launch) and H boxes: 32 rows x 64 bf16
+      const uint64_t rows_end = static_cast<uint64_t>(p.row0) + pr.rows;
+      const uint64_t zcols = pr.epi == Epi::SwigluFwd ? static_cast<uint64_t>(pr.N) : 2ULL * pr.N;
+      if (!make_map3s(&em.d, pr.D, false, zcols, rows_end, pr.nblk, pr.ldd * 2,
+                      static_cast<uint64_t>(p.rows_total) * pr.ldd * 2, 64, 32))
+        return cudaErrorInvalidValue;
+      if (pr.epi == Epi::SwigluFwd &&
+          !make_map3s(&em.d2, pr.D2, false, pr.N / 2, rows_end, pr.nblk, pr.ldd2 * 2,
+                      static_cast<uint64_t>(p.rows_total) * pr.ldd2 * 2, 64, 32))
+        return cudaErrorInvalidValue;
+      if (pr.epi == Epi::SwigluBwd &&
+          !make_map3s(&em.z, pr.Zin, false, zcols, rows_end, pr.nblk, pr.ldz * 2,
+                      static_cast<uint64_t>(p.rows_total) * pr.ldz * 2, 64, 32))
+        return cudaErrorInvalidValue;
+    }
     const bool tma_epi = pr.epi == Epi::StoreBF16 || pr.epi == Epi::StoreF32 ||
                          pr.epi == Epi::GeluFwd || pr.epi == Epi::GeluBwd;
     if (tma_epi) {

@@ -26,10 +26,12 @@
 // With fsmoe_peer_flags::wait_ns set, every wait adds the time it spent
 // spinning (globaltimer, first thread in to last flag seen) to that counter:
 // the untraced per-rank exposed-exchange time the bench reports.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 
 #include "capi_common.h"
 #include "kernels.h"
@@ -182,4 +184,72 @@ extern "C" int fsmoe_peer_wait(const fsmoe_peer_flags* f, int slot, unsigned lon
                                                                   target, f->wait_ns, f->timeout_ns);
   count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_peer_wait");
+}
+
+// ----------------------------------------------------- copy-engine exchange --
+// The chunked pipeline's dispatch-side exchanges (FSMoE's D_0..D_{r-1} on the
+// inter link, schedule_sim.cpp:182-216) without SM work: the permutation
+// kernel leaves the peers' rows in a canonical [E][C] send buffer, the copy
+// engines move pipeline chunk i (rows [lo, hi) of every block) into each
+// peer's receive buffer while the expert GEMMs of chunk i-1 hold every SM,
+// and a stream memory operation raises the chunk's arrival flag behind them.
+namespace {
+
+using PFN_writeValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+PFN_writeValue64 write_value_fn() {
+  static PFN_writeValue64 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue64", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_writeValue64>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+extern "C" int fsmoe_peer_copy_rows(const void* send, long long row_bytes, const fsmoe_peer_rows* dst,
+                                    long long lo, long long hi, int include_self, void* stream) {
+  if (!send || !dst || row_bytes <= 0 || lo < 0 || hi > dst->capacity || lo > hi)
+    return config_error("peer copy rows: send, map, row bytes > 0 and 0 <= lo <= hi <= capacity required");
+  if (dst->world < 1 || dst->world > MAX_PEERS || dst->rank < 0 || dst->rank >= dst->world)
+    return config_error("peer copy rows: world must be in [1, 8] and rank in [0, world)");
+  if (hi == lo) return FSMOE_OK;
+  const int P = dst->world, El = dst->experts_local, me = dst->rank;
+  const size_t pitch = static_cast<size_t>(dst->capacity * row_bytes);
+  const size_t width = static_cast<size_t>((hi - lo) * row_bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int k = 0; k < P; ++k) {
+    const int p = (me + k) % P;  // start with the next rank: spread the copies over the links
+    if (p == me && !include_self) continue;
+    if (!dst->base[p]) return config_error("peer copy rows: missing peer base");
+    // this rank's E_l blocks for p: send rows [(p El + el) C + lo, ... + hi)
+    const char* s = static_cast<const char*>(send) + (static_cast<size_t>(p) * El * dst->capacity + lo) * row_bytes;
+    // land in p's [rank][el][C] blocks
+    char* d = static_cast<char*>(dst->base[p]) + (static_cast<size_t>(me) * El * dst->capacity + lo) * row_bytes;
+    cudaError_t e = cudaMemcpy2DAsync(d, pitch, s, pitch, width, static_cast<size_t>(El),
+                                      cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "fsmoe_peer_copy_rows");
+  }
+  return FSMOE_OK;
+}
+
+extern "C" int fsmoe_peer_flag_write(const fsmoe_peer_flags* f, int slot, unsigned long long value,
+                                     void* stream) {
+  if (int rc = check_flags(f, slot)) return rc;
+  PFN_writeValue64 wv = write_value_fn();
+  if (!wv) return config_error("peer flag write: cuStreamWriteValue64 unavailable");
+  for (int p = 0; p < f->world; ++p) {
+    unsigned long long* a = f->base[p] + static_cast<long long>(slot) * f->world + f->rank;
+    // default flags: a system-scope memory fence orders the stream's earlier
+    // work (the copies) before the write
+    CUresult r = wv(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(a), value, 0);
+    if (r != CUDA_SUCCESS) return cuda_status(cudaErrorUnknown, "fsmoe_peer_flag_write");
+  }
+  return FSMOE_OK;
 }

@@ -121,6 +121,8 @@ def _worker(rank, world, port, precision, gate, ffn, rf, rb, transport, q):
     ("bf16", "expert_choice", "gated3", 2, 1, "peer"),
     ("bf16", "noisy_topk", "simple", 3, 2, "nccl"),
     ("f32", "cosine_topk", "simple", 1, 2, "nccl"),
+    ("bf16", "noisy_topk", "simple", 3, 2, "ce"),
+    ("f32", "sigmoid_topk", "gated3", 2, 3, "ce"),
 ])
 def test_ep_layer_matches_restatement(precision, gate, ffn, rf, rb, transport):
     import torch.multiprocessing as mp

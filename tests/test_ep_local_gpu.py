@@ -25,7 +25,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _run(world, precision, gate, ffn, rf, rb, k=2, dense=0, split=None, T=1024, M=256, H=256):
+def _run(world, precision, gate, ffn, rf, rb, k=2, dense=0, split=None, T=1024, M=256, H=256,
+         transport=None):
     import layer_oracle
     import pyoracle
     from paper_2501_10714_b200.layer import EpGroup, MoEConfig, MoELayer, expert_params, gate_params, run_ranks
@@ -47,9 +48,13 @@ def _run(world, precision, gate, ffn, rf, rb, k=2, dense=0, split=None, T=1024, 
         g = torch.Generator().manual_seed(900 + r)
         return torch.rand(dense, generator=g) * 2 - 1
 
-    old = os.environ.get("FSMOE_EP_SPLIT")
+    env = {}
     if split is not None:
-        os.environ["FSMOE_EP_SPLIT"] = str(split)
+        env["FSMOE_EP_SPLIT"] = str(split)
+    if transport is not None:
+        env["FSMOE_EP_TRANSPORT"] = transport
+    old = {k_: os.environ.get(k_) for k_ in env}
+    os.environ.update(env)
     try:
         groups = EpGroup.local_group(world, torch.cuda.current_device())
         layers = [None] * world
@@ -60,11 +65,11 @@ def _run(world, precision, gate, ffn, rf, rb, k=2, dense=0, split=None, T=1024, 
 
         caps = run_ranks(world, make)
     finally:
-        if split is not None:
-            if old is None:
-                os.environ.pop("FSMOE_EP_SPLIT", None)
+        for k_, v_ in old.items():
+            if v_ is None:
+                os.environ.pop(k_, None)
             else:
-                os.environ["FSMOE_EP_SPLIT"] = old
+                os.environ[k_] = v_
 
     def step(r):
         L = layers[r]
@@ -168,3 +173,16 @@ def test_local_ep_split_local_first():
     """FSMOE_EP_SPLIT: own experts' rows first, the peers' share on a second
     stream (moe_layer.cpp, the local-first split)."""
     _run(2, "bf16", "noisy_topk", "simple", 1, 1, split=1)
+
+
+@pytest.mark.parametrize("world,precision,gate,ffn,rf,rb,k", [
+    (2, "bf16", "noisy_topk", "simple", 3, 2, 2),
+    (4, "f32", "sigmoid_topk", "gated3", 2, 3, 2),
+    (8, "bf16", "noisy_topk", "simple", 4, 4, 1),
+    (4, "bf16", "expert_choice", "gated3", 1, 2, 2),
+])
+def test_local_ep_copy_engine_chunked_pipeline(world, precision, gate, ffn, rf, rb, k):
+    """FSMOE_EP_TRANSPORT=ce: the dispatch-side exchanges move per pipeline
+    chunk on the copy engines (fsmoe_peer_copy_rows) with stream-memory-op
+    flags (fsmoe_peer_flag_write), GEMM chunk i waiting only for chunk i."""
+    _run(world, precision, gate, ffn, rf, rb, k=k, transport="ce")
