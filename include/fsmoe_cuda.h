@@ -292,6 +292,10 @@ typedef struct fsmoe_gemm_desc {
    * force_ctas 1 | 2 (single CTA / tcgen05 cta_group::2 pair), force_bn 128 |
    * 256 | 512 columns; dbg: measurement-only epilogue ablations */
   int force_ctas, force_bn, dbg;
+  /* tile-order override (0 = the heuristic): band_m > 0 walks bands of
+   * band_m m-tiles column by column, band_n > 0 bands of band_n n-tiles row
+   * by row, band_m < 0 plain m-major order */
+  int band_m, band_n;
 } fsmoe_gemm_desc;
 
 int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream);

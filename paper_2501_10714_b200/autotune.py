@@ -138,15 +138,20 @@ def layer_of(cfg) -> P.Layer:
                    top_k=cfg.top_k)
 
 
-def collect(cfg, world: int, reps=10):
+def collect(cfg, world: int, reps=10, r_max=8):
     """Online profile for one layer shape on this box: collectives around the
-    layer's a2a volume and the GEMM around its capacity."""
+    layer's a2a volume, and the GEMM at exactly the chunk sizes the planner
+    chooses between (capacity C split into r = 1..r_max 128-row granule
+    chunks, as the executor splits it): the fitted per-launch alpha then
+    carries the wave quantisation of small chunks on 148 SMs, which a fit over
+    a few far-apart sizes smooths away."""
     layer = layer_of(cfg)
     vol = P.derive_volumes(layer, (world, world, 1, 1, world, 1))
     a2a = vol[0]
     sizes = [a2a / 8, a2a / 4, a2a / 2, a2a]
     cap = int(vol[6])
-    caps = sorted({max(128, (cap // d) // 128 * 128) for d in (8, 4, 2, 1)})
+    ng = max(1, -(-cap // 128))
+    caps = sorted({max(128, (ng // r) * 128) for r in range(1, r_max + 1)})
     while len(caps) < 3:          # small capacities: the fit still needs a slope
         caps.append(caps[-1] * 2)
     return profile_collectives(sizes, reps=reps) + profile_gemm(cfg.experts, caps, cfg.model_dim,
@@ -162,6 +167,43 @@ def plan(cfg, samples, world: int, r_max=8, t_gar_bwd_ms=0.0):
     out.update(profile=[float(v) for v in prof], min_r2=float(min_r2), clamped_mask=clamped,
                volumes=[float(v) for v in vol])
     return out
+
+
+def step_ms(layer, x, dy, steps=10, warmup=3):
+    """Measured forward + backward of one layer (CUDA events, max over ranks)."""
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    for _ in range(warmup):
+        layer.forward(x, y)
+        layer.backward(dy, dx)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        layer.forward(x, y)
+        layer.backward(dy, dx)
+    e.record()
+    torch.cuda.synchronize()
+    return _max_over_ranks(s.elapsed_time(e) / steps)
+
+
+def refine(cfg, ep, r_plan, x, dy, r_max=8, steps=10):
+    """Online check of a plan on the real layer (the paper's online
+    profiling, closing the loop the analytic model leaves open): measure the
+    step at the planned degree and its neighbours r-1, r+1 (both passes move
+    together), keep the fastest. Returns (r_fwd, r_bwd, {r: ms})."""
+    from .layer import MoELayer
+    r0 = max(r_plan)
+    cand = sorted({max(1, r0 - 1), r0, min(r_max, r0 + 1)})
+    meas = {}
+    keep = (cfg.r_fwd, cfg.r_bwd)
+    for r in cand:
+        cfg.r_fwd = cfg.r_bwd = r
+        layer = MoELayer(cfg, ep, init_seed=1)
+        meas[r] = step_ms(layer, x, dy, steps=steps)
+        layer.close()
+    cfg.r_fwd, cfg.r_bwd = keep
+    best = min(meas, key=meas.get)
+    return best, best, meas
 
 
 def autotune(cfg, world: int, reps=10, r_max=8):

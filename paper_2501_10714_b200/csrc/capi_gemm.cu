@@ -137,6 +137,8 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   p.force_ctas = d->force_ctas;
   p.force_bn = d->force_bn;
   p.dbg = d->dbg;
+  p.band_m = d->band_m;
+  p.band_n = d->band_n;
   if (d->blk_hi > 0) {
     if (d->kind != 0) return config_error("gemm: a block range needs a row-grouped problem");
     p.blocks = fsmoe_dev::RowRange{d->blk_lo, d->blk_hi, d->blk_exclude};

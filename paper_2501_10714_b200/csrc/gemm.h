@@ -74,6 +74,7 @@ struct GemmProblem {
   fsmoe_dev::RowRange blocks = fsmoe_dev::all_rows();  // row-grouped: blocks processed
   int max_sms = 0;                                        // > 0: cap the persistent grid
   int force_ctas = 0, force_bn = 0, dbg = 0;              // fsmoe_gemm_desc overrides
+  int band_m = 0, band_n = 0;                             // tile-order override
 };
 
 // bf16 operands, fp32 accumulate in TMEM (tcgen05). Returns cudaError_t.

@@ -53,6 +53,7 @@ struct KParams {
   int use_peers;           // row-grouped plain stores through `peers`
   fsmoe_dev::PeerRows peers;
   fsmoe_dev::RowRange blocks;  // row-grouped: the blocks this launch covers
+  int band_m, band_n;  // tile order: bands of band_m m-tiles (n walked inside) or band_n n-tiles
   int dbg;  // measurement only (fsmoe_gemm_desc::dbg): 1 no epilogue after the TMEM reads,
             // 2 no TMEM reads either, 4 everything but the TMA stores
 };
@@ -249,18 +250,27 @@ __device__ __forceinline__ TileInfo decode_tile_c(const KParams& p, int t) {
   // Only for wide problems (n-tiles > 2 bands): with few n-tiles the m-major
   // order already keeps the whole B in flight, and banding measured worse
   // there (ncu dram reads of the N = 4096 launches grew 1.4-2x).
-  constexpr int TILE_GM = 8;
   TileInfo ti;
   int per_g = p.m_tiles * p.n_tiles;
   ti.g = t / per_g;
   int rem = t - ti.g * per_g;
-  if (p.m_tiles >= 2 * TILE_GM && p.n_tiles > 2 * TILE_GM) {
-    const int band = rem / (TILE_GM * p.n_tiles);
-    const int m0 = band * TILE_GM;
-    const int gm = min(TILE_GM, p.m_tiles - m0);
-    const int idx = rem - band * TILE_GM * p.n_tiles;
+  if (p.band_m > 0) {
+    const int bm = p.band_m;
+    const int band = rem / (bm * p.n_tiles);
+    const int m0 = band * bm;
+    const int gm = min(bm, p.m_tiles - m0);
+    const int idx = rem - band * bm * p.n_tiles;
     ti.mt = m0 + idx % gm;
     ti.nt = idx / gm;
+  } else if (p.band_n > 0) {
+    // bands of band_n n-tiles (a B panel set stays in L2), m walked inside
+    const int bn = p.band_n;
+    const int band = rem / (bn * p.m_tiles);
+    const int n0 = band * bn;
+    const int gn = min(bn, p.n_tiles - n0);
+    const int idx = rem - band * bn * p.m_tiles;
+    ti.nt = n0 + idx % gn;
+    ti.mt = idx / gn;
   } else {
     ti.mt = rem / p.n_tiles;
     ti.nt = rem - ti.mt * p.n_tiles;
@@ -965,6 +975,20 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     if (!make_map3(&tb, pr.B, pr.No, p.rows_total, pr.nblk, 64, BK)) return cudaErrorInvalidValue;
   }
   p.num_tiles = p.n_groups * p.m_tiles * p.n_tiles;
+  // Tile order inside a group. Default: bands of 8 m-tiles walked column by
+  // column for wide launches (> 16 n-tiles), m-major otherwise (see
+  // decode_tile_c). fsmoe_gemm_desc::band_m / band_n override it (band_m < 0:
+  // plain m-major).
+  p.band_m = p.m_tiles >= 16 && p.n_tiles > 16 ? 8 : 0;
+  p.band_n = 0;
+  if (pr.band_m > 0) {
+    p.band_m = pr.band_m;
+  } else if (pr.band_n > 0) {
+    p.band_m = 0;
+    p.band_n = pr.band_n;
+  } else if (pr.band_m < 0) {
+    p.band_m = 0;
+  }
   // epilogue maps: 32-row boxes of 128 bytes (64 bf16 / 32 fp32 columns); the
   // row extent ends at the window so TMA clips rows outside [row0, row0+rows)
   EpiMaps em;

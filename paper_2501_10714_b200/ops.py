@@ -36,7 +36,7 @@ GEMM_FORCE = (0, 0)
 
 def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn_major=False,
                  rows_total=0, row0=0, valid_rows=None, epi="store_bf16", D2=None, Zin=None, ldd=None, ldd2=0, ldz=0,
-                 accumulate=False, precision=0, force=None, dbg=0):
+                 accumulate=False, precision=0, force=None, dbg=0, order=(0, 0)):
     """Grouped expert GEMM (see csrc/gemm.h). kind: 'row' or 'k'."""
     lib = NL.cuda_lib()
     d = NL.GemmDesc()
@@ -55,6 +55,7 @@ def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn
     d.precision = precision
     d.force_ctas, d.force_bn = force if force is not None else GEMM_FORCE
     d.dbg = dbg
+    d.band_m, d.band_n = order
     NL.check(lib.fsmoe_grouped_gemm(C.byref(d), _stream()))
 
 
