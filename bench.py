@@ -361,17 +361,45 @@ def timeline_summary(trace: str, steps: int):
             "note": "traced run synchronises per phase call; shares, not absolute step time"}
 
 
-def make_layer(W, args, world, rank, ep, gate=None):
-    from paper_2501_10714_b200.layer import MoEConfig, MoELayer
+def layer_config(W, gate=None, r_fwd=1, r_bwd=1, transport=""):
+    from paper_2501_10714_b200.layer import MoEConfig
     gate = gate or W["gate"].split()[0]
     # expert choice: every expert takes C = k f T / E tokens (workload.cpp:156-171,
     # the layer derives C from k); cosine: a 64-row projection (the reference
     # leaves the dimension open)
-    cfg = MoEConfig(tokens=W["tokens_per_gpu"], model_dim=W["d_model"], ffn_dim=W["d_ffn"],
-                    experts=W["experts"], top_k=W["top_k"], gate=gate, ffn=W["ffn"].split()[0],
-                    capacity_factor=W["capacity_factor"], proj_dim=64 if gate == "cosine_topk" else 0,
-                    precision="bf16", seed=7, r_fwd=args.r_fwd, r_bwd=args.r_bwd)
-    return MoELayer(cfg, ep, init_seed=1)
+    return MoEConfig(tokens=W["tokens_per_gpu"], model_dim=W["d_model"], ffn_dim=W["d_ffn"],
+                     experts=W["experts"], top_k=W["top_k"], gate=gate, ffn=W["ffn"].split()[0],
+                     capacity_factor=W["capacity_factor"], proj_dim=64 if gate == "cosine_topk" else 0,
+                     precision="bf16", seed=7, r_fwd=r_fwd, r_bwd=r_bwd, transport=transport)
+
+
+def make_layer(W, args, world, rank, ep, gate=None, pipe=None):
+    from paper_2501_10714_b200.layer import MoELayer
+    rf, rb, tr = pipe or (max(args.r_fwd, 1), max(args.r_bwd, 1), args.transport)
+    return MoELayer(layer_config(W, gate, rf, rb, tr), ep, init_seed=1)
+
+
+def choose_pipeline(W, args, world, rank, ep, gate, x, dy):
+    """FSMoE's online profiling on this box (paper_2501_10714_b200.autotune):
+    collectives + GEMM chunks -> bench CSV -> fit_profile -> plan_layer (the
+    reference's planner), then the plan and its neighbours measured on the
+    real layer for each EP transport; the fastest is used. Explicit
+    --r-fwd / --r-bwd / --transport skip it. Returns ((r_fwd, r_bwd,
+    transport), report)."""
+    if world == 1:
+        return (max(args.r_fwd, 1), max(args.r_bwd, 1), args.transport), {"how": "N = 1: no exchange, r = 1"}
+    if args.r_fwd > 0 and args.r_bwd > 0:
+        return (args.r_fwd, args.r_bwd, args.transport), {"how": "given on the command line"}
+    from paper_2501_10714_b200 import autotune
+    cfg = layer_config(W, gate)
+    samples, _ = autotune.collect(cfg, world, r_max=4)
+    p = autotune.plan(cfg, samples, world, r_max=4)
+    trs = (args.transport,) if args.transport else ("peer", "ce")
+    rf, rb, meas = autotune.refine(cfg, ep, (p["r_fwd"], p["r_bwd"]), x, dy, r_max=4, steps=5, transports=trs)
+    rep = {"how": "on-box profile -> fit_profile -> plan_layer -> refined on the layer (autotune.refine)",
+           "planned": [p["r_fwd"], p["r_bwd"]], "chosen": [rf, rb, cfg.transport],
+           "refine_ms": {f"{k[0]}:r{k[1]}": round(v, 4) for k, v in meas.items()}}
+    return (rf, rb, cfg.transport), rep
 
 
 def timed_steps(layer, x, y, dy, dx, args, world, warm_seconds):
@@ -444,12 +472,13 @@ def gpu_arm(args):
                   WORKLOAD["experts"])
     gate = args.gate or WORKLOAD["gate"].split()[0]
     ep = EpGroup(world, rank, local, max_ctas=args.nccl_ctas) if world > 1 else None
-    layer = make_layer(WORKLOAD, args, world, rank, ep, gate)
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     x = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
     dy = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
     dx = torch.empty_like(x)
     y = torch.empty_like(x)
+    pipe, pipe_rep = choose_pipeline(WORKLOAD, args, world, rank, ep, gate, x, dy)
+    layer = make_layer(WORKLOAD, args, world, rank, ep, gate, pipe=pipe)
     ms, extra_warm, clk, launches, wait_ms = timed_steps(layer, x, y, dy, dx, args, world,
                                                          args.warm_seconds)
     value = world * T / (ms * 1e-3)
@@ -610,10 +639,11 @@ def gpu_arm(args):
     extra = None
     if args.config == "mixtral" and not args.no_extra:
         W1 = WORKLOADS["gpt2m"]
-        l1 = make_layer(W1, args, world, rank, ep)
         T1, M1 = W1["tokens_per_gpu"], W1["d_model"]
         x1 = torch.randn(T1, M1, device="cuda", generator=g).to(torch.bfloat16)
         dy1 = torch.randn(T1, M1, device="cuda", generator=g).to(torch.bfloat16)
+        pipe1, pipe1_rep = choose_pipeline(W1, args, world, rank, ep, None, x1, dy1)
+        l1 = make_layer(W1, args, world, rank, ep, pipe=pipe1)
         ms1, ex1, clk1, _, wait1 = timed_steps(l1, x1, torch.empty_like(x1), dy1, torch.empty_like(x1),
                                                args, world, 1.0)
         extra = {"workload": W1["workload"], "value": world * T1 / (ms1 * 1e-3), "unit": "tokens/s",
@@ -643,7 +673,8 @@ def gpu_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random tokens, random-init experts)",
-            "config": dict(WORKLOAD, parallelism=f"ep{world}", r_fwd=args.r_fwd, r_bwd=args.r_bwd,
+            "config": dict(WORKLOAD, parallelism=f"ep{world}", r_fwd=pipe[0], r_bwd=pipe[1],
+                           transport=(pipe[2] or "peer") if world > 1 else None, pipeline=pipe_rep,
                            capacity=C, warmup_extra_steps=extra_warm,
                            warmup_note=f"W warm-up steps, then more until {args.warm_seconds:.0f} s "
                                        "of stepping (steady clocks)",
@@ -669,8 +700,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--r-fwd", type=int, default=1)
-    ap.add_argument("--r-bwd", type=int, default=1)
+    ap.add_argument("--r-fwd", type=int, default=0, help="pipeline degree (0: FSMoE's online plan at N > 1)")
+    ap.add_argument("--r-bwd", type=int, default=0)
+    ap.add_argument("--transport", default="", choices=["", "peer", "ce", "nccl"],
+                    help="EP exchange ('' = chosen with the pipeline degree, or FSMOE_EP_TRANSPORT)")
     ap.add_argument("--nccl-ctas", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")

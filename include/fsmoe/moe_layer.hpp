@@ -38,6 +38,9 @@ struct MoELayerConfig {
   int device = 0;
   long long dense_grad_elems = 0;  // optional replicated-gradient buffer (fp32)
   std::vector<long long> ar_slices;  // allreduce slice sizes (elements); empty -> one
+  // EP exchange: 0 = FSMOE_EP_TRANSPORT or peer, 1 = peer stores fused into
+  // the producers, 2 = ce (chunked copy-engine dispatch), 3 = nccl send/recv
+  int transport = 0;
 };
 
 class EpGroup;  // NCCL communicator over the expert-parallel ranks

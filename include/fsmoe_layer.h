@@ -41,6 +41,10 @@ typedef struct fsmoe_layer_config {
    * this factor (<= 0 means 1.0), or k * tokens when unlimited != 0 */
   double capacity_factor;
   int unlimited;
+  /* EP exchange (P > 1): 0 = FSMOE_EP_TRANSPORT or "peer", 1 peer (row stores
+   * fused into the producing kernels), 2 ce (FSMoE's chunked pipeline on the
+   * copy engines for the dispatch side), 3 nccl (grouped send/recv) */
+  int transport;
 } fsmoe_layer_config;
 
 typedef struct fsmoe_layer_params {

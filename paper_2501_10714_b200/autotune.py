@@ -114,9 +114,11 @@ def profile_collectives(sizes, dtype=torch.bfloat16, reps=10):
     return out
 
 
-def profile_gemm(nblk, caps, M, H, reps=10):
+def profile_gemm(nblk, caps, M, H, reps=10, unit_h=None):
     """Expert-GEMM samples: one grouped launch over the layer's nblk blocks of
-    c rows (c in caps), K = M, N = H; n = c*M*H (the planner's unit)."""
+    c rows (c in caps), K = M, N = H; n = c*M*unit_h (the planner's MAC unit,
+    unit_h = hidden_scale * M; H by default)."""
+    unit_h = unit_h or H
     out = []
     bf = torch.bfloat16
     for c in caps:
@@ -124,15 +126,21 @@ def profile_gemm(nblk, caps, M, H, reps=10):
         W = (torch.randn(nblk, H, M, device="cuda") / math.sqrt(M)).to(bf)
         Z = torch.empty(nblk, c, H, device="cuda", dtype=bf)
         fn = lambda: ops.grouped_gemm("row", X, W, Z, nblk=nblk, rows=c, K=M, N=H, n_w=nblk)  # noqa: E731
-        out.append(("gemm", float(c) * M * H, _max_over_ranks(_time_ms(fn, reps))))
+        out.append(("gemm", float(c) * M * unit_h, _max_over_ranks(_time_ms(fn, reps))))
     return out
+
+
+def hidden_scale(cfg) -> int:
+    """The reference's integer LayerConfig::hidden_scale (H = hidden_scale * M,
+    workload.hpp:20) nearest to the layer's H / M (Mixtral: 14336 / 4096 = 3.5
+    -> 4). The GEMM samples are recorded in the same planner unit
+    (profile_gemm), so the fitted slope absorbs the difference."""
+    return max(1, int(round(cfg.ffn_dim / cfg.model_dim)))
 
 
 def layer_of(cfg) -> P.Layer:
     """MoEConfig -> the planner's LayerConfig (B = 1, L = local tokens)."""
-    hs = cfg.ffn_dim // cfg.model_dim
-    if hs * cfg.model_dim != cfg.ffn_dim:
-        raise ValueError("planner needs ffn_dim = hidden_scale * model_dim")
+    hs = hidden_scale(cfg)
     return P.Layer(batch=1, heads=1, seq_len=cfg.tokens, model_dim=cfg.model_dim, hidden_scale=hs,
                    capacity_factor=cfg.capacity_factor, ffn=cfg.ffn, experts=cfg.experts,
                    top_k=cfg.top_k)
@@ -154,8 +162,9 @@ def collect(cfg, world: int, reps=10, r_max=8):
     caps = sorted({max(128, (ng // r) * 128) for r in range(1, r_max + 1)})
     while len(caps) < 3:          # small capacities: the fit still needs a slope
         caps.append(caps[-1] * 2)
-    return profile_collectives(sizes, reps=reps) + profile_gemm(cfg.experts, caps, cfg.model_dim,
-                                                                cfg.ffn_dim, reps=reps), vol
+    return profile_collectives(sizes, reps=reps) + profile_gemm(
+        cfg.experts, caps, cfg.model_dim, cfg.ffn_dim, reps=reps,
+        unit_h=hidden_scale(cfg) * cfg.model_dim), vol
 
 
 def plan(cfg, samples, world: int, r_max=8, t_gar_bwd_ms=0.0):
@@ -186,23 +195,38 @@ def step_ms(layer, x, dy, steps=10, warmup=3):
     return _max_over_ranks(s.elapsed_time(e) / steps)
 
 
-def refine(cfg, ep, r_plan, x, dy, r_max=8, steps=10):
+def refine(cfg, ep, r_plan, x, dy, r_max=8, steps=10, transports=None):
     """Online check of a plan on the real layer (the paper's online
     profiling, closing the loop the analytic model leaves open): measure the
     step at the planned degree and its neighbours r-1, r+1 (both passes move
-    together), keep the fastest. Returns (r_fwd, r_bwd, {r: ms})."""
+    together), keep the fastest. With `transports` (EP only) every candidate
+    degree is tried on each transport ("peer" only at r = 1 and the plan's r:
+    its dispatch does not pipeline). Returns (r_fwd, r_bwd, {key: ms}) with
+    key = r, or (transport, r) when transports are given; cfg.transport is
+    set to the winner's."""
     from .layer import MoELayer
     r0 = max(r_plan)
-    cand = sorted({max(1, r0 - 1), r0, min(r_max, r0 + 1)})
+    rs = sorted({max(1, r0 - 1), r0, min(r_max, r0 + 1)})
+    if transports:
+        # the copy-engine pipeline needs r >= 2 to overlap anything: try 2 too
+        ce_rs = sorted({r for r in rs + [2] if 2 <= r <= r_max})
+        cand = [(t, r) for t in transports for r in (sorted({1, r0}) if t == "peer" else ce_rs)]
+    else:
+        cand = rs
     meas = {}
-    keep = (cfg.r_fwd, cfg.r_bwd)
-    for r in cand:
+    keep = (cfg.r_fwd, cfg.r_bwd, cfg.transport)
+    for c in cand:
+        t, r = c if transports else (cfg.transport, c)
         cfg.r_fwd = cfg.r_bwd = r
+        cfg.transport = t
         layer = MoELayer(cfg, ep, init_seed=1)
-        meas[r] = step_ms(layer, x, dy, steps=steps)
+        meas[c] = step_ms(layer, x, dy, steps=steps)
         layer.close()
-    cfg.r_fwd, cfg.r_bwd = keep
+    cfg.r_fwd, cfg.r_bwd, cfg.transport = keep
     best = min(meas, key=meas.get)
+    if transports:
+        cfg.transport = best[0]
+        return best[1], best[1], meas
     return best, best, meas
 
 

@@ -129,6 +129,7 @@ int fsmoe_layer_create(const fsmoe_layer_config* c, fsmoe_ep* ep, fsmoe_layer** 
     cfg.capacity = c->capacity;
     cfg.capacity_factor = c->capacity_factor > 0.0 ? c->capacity_factor : 1.0;
     cfg.unlimited_capacity = c->unlimited != 0;
+    cfg.transport = c->transport;
     cfg.proj_dim = c->proj_dim;
     cfg.seed = c->seed;
     cfg.precision = c->precision ? fsmoe::Precision::f32 : fsmoe::Precision::bf16;

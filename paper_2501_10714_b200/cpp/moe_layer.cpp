@@ -643,9 +643,13 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
   I.fill = static_cast<long long*>(I.dalloc("fill", 8 * E));
   I.dropped = static_cast<long long*>(I.dalloc("dropped", 8));
   if (I.P > 1) {
+    // MoELayerConfig::transport, else FSMOE_EP_TRANSPORT, else the peer stores
     const char* tr = std::getenv("FSMOE_EP_TRANSPORT");
-    I.peer = !(tr && std::strcmp(tr, "nccl") == 0);
-    I.ce = tr && std::strcmp(tr, "ce") == 0;
+    int t = cfg.transport;
+    if (t == 0) t = !tr ? 1 : std::strcmp(tr, "nccl") == 0 ? 3 : std::strcmp(tr, "ce") == 0 ? 2 : 1;
+    if (t < 1 || t > 3) throw ConfigError("layer: transport must be 0 (default), 1 peer, 2 ce or 3 nccl");
+    I.peer = t != 3;
+    I.ce = t == 2;
     if (!I.peer && ep->local())
       throw ConfigError("layer: the NCCL transport needs one GPU per rank (local group given)");
   }

@@ -26,7 +26,7 @@ class LayerConfigC(C.Structure):
         ("precision", C.c_int), ("r_fwd", C.c_int), ("r_bwd", C.c_int), ("device", C.c_int),
         ("dense_grad_elems", C.c_longlong), ("n_ar_slices", C.c_int),
         ("ar_slices", C.POINTER(C.c_longlong)), ("capacity_factor", C.c_double),
-        ("unlimited", C.c_int),
+        ("unlimited", C.c_int), ("transport", C.c_int),
     ]
 
 
@@ -47,6 +47,7 @@ class MoEConfig:
     capacity: int = 0            # 0 -> capacity_tokens(k, capacity_factor, unlimited)
     capacity_factor: float = 1.0
     unlimited: bool = False
+    transport: str = ""          # "" (FSMOE_EP_TRANSPORT or peer), "peer", "ce", "nccl"
     proj_dim: int = 0
     seed: int = 7
     precision: str = "bf16"      # or "f32" (check mode)
@@ -218,6 +219,7 @@ class MoELayer:
         c.capacity = 0  # the C++ side derives it (capacity_tokens, workload.cpp:43-51)
         c.capacity_factor = cfg.capacity_factor
         c.unlimited = 1 if cfg.unlimited else 0
+        c.transport = {"": 0, "peer": 1, "ce": 2, "nccl": 3}[cfg.transport]
         if cfg.capacity:
             c.capacity = cfg.capacity
         c.proj_dim = cfg.proj_dim
