@@ -477,7 +477,11 @@ def gpu_arm(args):
     dy = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
     dx = torch.empty_like(x)
     y = torch.empty_like(x)
-    pipe, pipe_rep = choose_pipeline(WORKLOAD, args, world, rank, ep, gate, x, dy)
+    try:
+        pipe, pipe_rep = choose_pipeline(WORKLOAD, args, world, rank, ep, gate, x, dy)
+    except Exception as exc:  # the planning step only picks r / transport: fall back to r = 1
+        pipe, pipe_rep = (1, 1, args.transport), {"how": f"planning failed ({exc!r}); r = 1"}
+        torch.cuda.synchronize()
     layer = make_layer(WORKLOAD, args, world, rank, ep, gate, pipe=pipe)
     ms, extra_warm, clk, launches, wait_ms = timed_steps(layer, x, y, dy, dx, args, world,
                                                          args.warm_seconds)
@@ -642,12 +646,16 @@ def gpu_arm(args):
         T1, M1 = W1["tokens_per_gpu"], W1["d_model"]
         x1 = torch.randn(T1, M1, device="cuda", generator=g).to(torch.bfloat16)
         dy1 = torch.randn(T1, M1, device="cuda", generator=g).to(torch.bfloat16)
-        pipe1, pipe1_rep = choose_pipeline(W1, args, world, rank, ep, None, x1, dy1)
+        try:
+            pipe1, pipe1_rep = choose_pipeline(W1, args, world, rank, ep, None, x1, dy1)
+        except Exception as exc:
+            pipe1, pipe1_rep = (1, 1, args.transport), {"how": f"planning failed ({exc!r}); r = 1"}
         l1 = make_layer(W1, args, world, rank, ep, pipe=pipe1)
         ms1, ex1, clk1, _, wait1 = timed_steps(l1, x1, torch.empty_like(x1), dy1, torch.empty_like(x1),
                                                args, world, 1.0)
         extra = {"workload": W1["workload"], "value": world * T1 / (ms1 * 1e-3), "unit": "tokens/s",
-                 "ms_per_step": ms1, "steps": args.steps, "capacity": l1.capacity, "clocks": clk1}
+                 "ms_per_step": ms1, "steps": args.steps, "capacity": l1.capacity, "clocks": clk1,
+                 "r_fwd": pipe1[0], "r_bwd": pipe1[1], "pipeline": pipe1_rep}
         if world > 1:
             per1 = [None] * world
             dist.all_gather_object(per1, wait1)
