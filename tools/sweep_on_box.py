@@ -52,9 +52,11 @@ def fwd_bwd_ms(layer, x, dy, steps=10, warmup=3):
     return out[0], out[1] - out[0]
 
 
-def grid(quick):
+def grid(quick, wide=False):
     if quick:
         return [(4096, 1024, 2, 8, 2), (16384, 1024, 4, 16, 1)]
+    if wide:  # round 2: the C4 corners round 1 left out (T 64k, E 64, M 4096)
+        return list(itertools.product((4096, 16384, 65536), (1024, 4096), (4,), (8, 64), (1, 2)))
     pts = []
     for T, M, hs, E, k in itertools.product((4096, 16384), (1024, 2048), (2, 4), (8, 32), (1, 2)):
         pts.append((T, M, hs, E, k))
@@ -66,7 +68,8 @@ def main():
     ap.add_argument("--out", default="gpurun_out/sweep")
     ap.add_argument("--r-max", type=int, default=4)
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--transports", default="peer,nccl")
+    ap.add_argument("--wide", action="store_true")
+    ap.add_argument("--transports", default="peer,ce")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -81,7 +84,7 @@ def main():
     transports = [t for t in args.transports.split(",") if world > 1 or t == "peer"]
     rows = []
     t0 = time.time()
-    for (T, M, hs, E, k) in grid(args.quick):
+    for (T, M, hs, E, k) in grid(args.quick, args.wide):
         if E % world:
             continue
         cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=hs * M, experts=E, top_k=k,
@@ -98,18 +101,24 @@ def main():
         x = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
         dy = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
         meas = {}
+        ep = EpGroup(world, rank, local, max_ctas=16) if world > 1 else None
         for tr in transports:
-            os.environ["FSMOE_EP_TRANSPORT"] = tr
-            ep = EpGroup(world, rank, local, max_ctas=16) if world > 1 else None
+            cfg.transport = tr
             m = {}
             for r in range(1, args.r_max + 1):
                 cfg.r_fwd = cfg.r_bwd = r
                 layer = MoELayer(cfg, ep, init_seed=1)
                 m[r] = fwd_bwd_ms(layer, x, dy)
                 layer.close()
-            if ep:
-                ep.close()
             meas[tr] = m
+        # FSMoE's online loop as bench.py runs it: the plan refined on the layer
+        cfg.transport = ""
+        rf, rb, cand = autotune.refine(cfg, ep, (p["r_fwd"], p["r_bwd"]), x, dy, r_max=args.r_max,
+                                       steps=5, transports=tuple(transports) if world > 1 else None)
+        refined = {"transport": cfg.transport or "peer", "r": rf,
+                   "candidates_ms": {str(c): v for c, v in cand.items()}}
+        if ep:
+            ep.close()
         del x, dy
         torch.cuda.empty_cache()
         row = {"T": T, "M": M, "H": hs * M, "E": E, "k": k, "capacity": int(vol[6]),
@@ -117,7 +126,13 @@ def main():
                         "case_bwd": p["case_bwd"], "t_moe_fwd_ms": p["t_moe_fwd_ms"],
                         "t_moe_bwd_ms": p["t_moe_bwd_ms"], "min_r2": p["min_r2"]},
                "predicted_ms": {r: v for r, v in pred.items()},
-               "measured_ms": {tr: {r: v for r, v in m.items()} for tr, m in meas.items()}}
+               "measured_ms": {tr: {r: v for r, v in m.items()} for tr, m in meas.items()},
+               "refined": refined}
+        step = {(tr, r): v[0] + v[1] for tr, m in meas.items() for r, v in m.items()}
+        best = min(step, key=step.get)
+        row["best_step"] = {"transport": best[0], "r": best[1], "ms": step[best],
+                            "refined_over_best": step[(refined["transport"], refined["r"])] / step[best],
+                            "plan_peer_over_best": step[(transports[0], max(p["r_fwd"], p["r_bwd"]))] / step[best]}
         for tr, m in meas.items():
             bf = min(m, key=lambda r: m[r][0])
             bb = min(m, key=lambda r: m[r][1])
@@ -126,7 +141,7 @@ def main():
                                  "plan_bwd_over_best": m[p["r_bwd"]][1] / m[bb][1]}
         rows.append(row)
         if rank == 0:
-            print(json.dumps({k_: row[k_] for k_ in ("T", "M", "H", "E", "k", "plan")}
+            print(json.dumps({k_: row[k_] for k_ in ("T", "M", "H", "E", "k", "plan", "best_step")}
                              | {f"best_{tr}": row[f"best_{tr}"] for tr in meas},
                              default=float), flush=True)
     if rank == 0:
