@@ -71,7 +71,8 @@ def summarise(path):
     ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
     ui = h.index("Metric Unit")
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+             "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
     per = {}
     for r in rows[hi + 1:]:
         if len(r) <= vi or "grouped_gemm" not in r[ki]:
