@@ -37,6 +37,7 @@
 
 #include "host_once.h"
 #include "capi_common.h"
+#include "gemm.h"
 #include "glibc_libm.cuh"
 #include "kernels.h"
 #include "route_common.cuh"
@@ -57,9 +58,12 @@ __device__ __forceinline__ float load_as_float(const void* base, long long i) {
 }
 
 // W32[j][c], WT[c][j] for c < Ea from Wa, else from Wb; wn[c] = |column|_2 (upper bound).
+// Wtc (optional): the tensor-core screen's B operand [128][M] bf16, K-major:
+// row c = bf16(W[:, c]) (hi), row NC + c = bf16(W[:, c] - hi) (lo).
 __global__ void w_prep_kernel(int M, int Ea, const double* __restrict__ Wa, int Eb,
                               const double* __restrict__ Wb, float* __restrict__ W32,
-                              double* __restrict__ WT, double* __restrict__ wn) {
+                              double* __restrict__ WT, double* __restrict__ wn,
+                              __nv_bfloat16* __restrict__ Wtc) {
   const int NC = Ea + Eb;
   const int c = blockIdx.x;
   double ss = 0.0;
@@ -79,6 +83,11 @@ __global__ void w_prep_kernel(int M, int Ea, const double* __restrict__ Wa, int 
       if (j >= M) break;
       W32[static_cast<long long>(j) * NC + c] = static_cast<float>(v[u]);
       WT[static_cast<long long>(c) * M + j] = v[u];
+      if (Wtc) {
+        const __nv_bfloat16 h = __double2bfloat16(v[u]);
+        Wtc[static_cast<long long>(c) * M + j] = h;
+        Wtc[static_cast<long long>(NC + c) * M + j] = __double2bfloat16(v[u] - static_cast<double>(__bfloat162float(h)));
+      }
       ss = __fma_rn(v[u], v[u], ss);
     }
   }
@@ -822,6 +831,129 @@ __global__ void __launch_bounds__(512 + SC_MT_WARPS * 32)
   }
 }
 
+// ------------------------------------------------- tensor-core screen --
+// The approximate scores of the fused path on the tensor cores: one tcgen05
+// GEMM P = x . [W_hi | W_lo] (bf16 operands, exact products, fp32 TMEM
+// accumulation; W_hi = bf16(W), W_lo = bf16(W - W_hi)), then
+// `screen_tc_kernel` turns P into s~ = P_hi + P_lo and applies the same
+// noise / bound / candidate logic as `screen_kernel`. The bound covers:
+// the hi/lo split residual |W - W_hi - W_lo| <= 2^-18 |W|, the tensor core's
+// fp32 accumulation at up to two ulps per addition in any order
+// (gamma' = M 2^-22 / (1 - M 2^-22), on |x| . (|W_hi| + |W_lo|) <=
+// (1 + 2^-8) |x| . |W|), and the reference's own fp64 sequential rounding —
+// all times |x|_2 |W_e|_2 (Cauchy-Schwarz), as before.
+constexpr int TC_COLS = 128;  // GEMM output columns (2 NC <= 128)
+constexpr int ST_TOK = 32;    // tokens per screen_tc block (4 threads each + one noise-draw warp)
+constexpr int ST_MAIN = 4 * ST_TOK;
+
+template <int KIND, int E_MAX>
+__global__ void __launch_bounds__(ST_MAIN + 32)
+    screen_tc_kernel(const __nv_bfloat16* __restrict__ x, int T, int M, int E, int k,
+                     const float* __restrict__ P, const double* __restrict__ wn, double cB,
+                     double gam, uint64_t seed, double* __restrict__ noise_ws,
+                     double* __restrict__ scores_out, double* __restrict__ spread_out,
+                     uint64_t* __restrict__ mask) {
+  __shared__ uint64_t draws[KIND == 0 ? ST_TOK * 2 * E_MAX : 1];
+  __shared__ float nrm[ST_TOK * 4];
+  __shared__ double lo[ST_TOK * E_MAX], hi[ST_TOK * E_MAX];
+  const int tid = threadIdx.x;
+  const int t0 = blockIdx.x * ST_TOK;
+  const int ntok = min(ST_TOK, T - t0);
+  const int NC = KIND == 0 ? 2 * E : E;
+  if (tid >= ST_MAIN) {
+    // noise-draw warp (as screen_kernel): the first 2E outputs of mt19937_64(seed + t)
+    const int mt_tid = tid - ST_MAIN;
+    if (KIND == 0)
+      for (int tl = mt_tid; tl < ntok; tl += 32) {
+        uint64_t lw[2 * E_MAX + 1];
+        uint64_t w = seed + static_cast<uint64_t>(t0 + tl);
+        lw[0] = w;
+        const int nout = 2 * E;
+        for (int i = 1; i <= nout; ++i) {
+          w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+          lw[i] = w;
+        }
+        for (int i = nout + 1; i < 156; ++i) w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(i);
+        for (int o = 0; o < nout; ++o) {
+          w = 6364136223846793005ULL * (w ^ (w >> 62)) + static_cast<uint64_t>(156 + o);
+          const uint64_t y = (lw[o] & MT_UM) | (lw[o + 1] & MT_LM);
+          draws[tl * 2 * E_MAX + o] = temper(w ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL));
+        }
+      }
+  } else {
+    // |x_t|^2 from the exact squares of the bf16 values: four threads per
+    // token, each a quarter of the row (16-byte loads)
+    const int tl = tid >> 2, q = tid & 3;
+    float nacc = 0.f;
+    if (tl < ntok) {
+      const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<long long>(t0 + tl) * M);
+      const int nv = M / 8;
+      for (int v = q; v < nv; v += 4) {
+        const uint4 u = xr[v];
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float a = __uint_as_float(w4[c] << 16), b = __uint_as_float(w4[c] & 0xffff0000u);
+          nacc = fmaf(a, a, nacc);
+          nacc = fmaf(b, b, nacc);
+        }
+      }
+    }
+    nrm[tid] = nacc;
+  }
+  __syncthreads();
+  for (int pi = tid; pi < ntok * E; pi += blockDim.x) {
+    const int tl = pi / E, e = pi % E;
+    const long long o = static_cast<long long>(t0 + tl) * E + e;
+    const double xs2 = (static_cast<double>(nrm[4 * tl]) + static_cast<double>(nrm[4 * tl + 1])) +
+                       (static_cast<double>(nrm[4 * tl + 2]) + static_cast<double>(nrm[4 * tl + 3]));
+    const double xnorm = sqrt(xs2 * (1.0 + 2.0 * gam)) * (1.0 + 1e-12);
+    const float* pr = P + static_cast<long long>(t0 + tl) * TC_COLS;
+    const double r = static_cast<double>(pr[e]) + static_cast<double>(pr[NC + e]);
+    const double br = cB * xnorm * wn[e];
+    double sv, bnd;
+    if (KIND == 0) {
+      const double sp = static_cast<double>(pr[E + e]) + static_cast<double>(pr[NC + E + e]);
+      const uint64_t o0 = draws[tl * 2 * E_MAX + 2 * e];
+      const uint64_t o1 = draws[tl * 2 * E_MAX + 2 * e + 1];
+      const double u1 = __dmul_rn(__dadd_rn(static_cast<double>(o0 >> 11), 0.5), 0x1.0p-53);
+      const double u2 = __dmul_rn(__dadd_rn(static_cast<double>(o1 >> 11), 0.5), 0x1.0p-53);
+      const double n = fsmoe_libm::gl_normal(u1, u2);
+      const double bs = cB * xnorm * wn[E + e];
+      const double soft = log1p(exp(sp));
+      sv = r + n * soft;
+      bnd = br + fabs(n) * bs + 1e-12 * (fabs(r) + fabs(n * soft)) + 1e-300;
+      noise_ws[o] = n;
+      if (spread_out) spread_out[o] = sp;
+    } else {
+      sv = r;
+      bnd = br + 1e-12 * fabs(r) + 1e-300;
+    }
+    if (scores_out) scores_out[o] = sv;
+    lo[tl * E_MAX + e] = sv - bnd;
+    hi[tl * E_MAX + e] = sv + bnd;
+  }
+  __syncthreads();
+  // candidates: upper bound reaches the k-th largest lower bound
+  if (tid < ntok) {
+    const double* l = lo + tid * E_MAX;
+    const double* h = hi + tid * E_MAX;
+    uint64_t taken = 0;
+    double kth = 0.0;
+    for (int j = 0; j < k; ++j) {
+      int bi = -1;
+      for (int e = 0; e < E; ++e)
+        if (!((taken >> e) & 1ULL) && (bi < 0 || l[e] > l[bi])) bi = e;
+      taken |= 1ULL << bi;
+      kth = l[bi];
+    }
+    uint64_t m = 0;
+    for (int e = 0; e < E; ++e)
+      if (h[e] >= kth) m |= 1ULL << e;
+    mask[t0 + tid] = m;
+  }
+}
+
 constexpr int XF_TOK = 64;       // tokens per exact/final block
 constexpr int XF_THREADS = 512;
 constexpr int XF_JC = 64;        // columns per stage
@@ -1186,7 +1318,48 @@ void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const floa
   ::fsmoe::count_launch();
 }
 
+template <int KIND, int E_MAX>
+void launch_fused_tc(const fsmoe_gate_desc& d, const void* x, const __nv_bfloat16* Wtc, float* P,
+                     const double* WT, const double* wn, double* noise_ws, uint64_t* mask,
+                     int* pick_token, int* pick_expert, double* pick_weight, double* scores_out,
+                     double* spread_out, cudaStream_t st) {
+  const int T = d.tokens, M = d.model_dim, E = d.score_cols, k = d.top_k;
+  GemmProblem g;
+  g.kind = GemmKind::RowGrouped;
+  g.nblk = 1;
+  g.rows = g.rows_total = T;
+  g.K = M;
+  g.N = TC_COLS;
+  g.n_w = 1;
+  g.A = x;
+  g.B = Wtc;
+  g.epi = Epi::StoreF32;
+  g.D = P;
+  g.ldd = TC_COLS;
+  g.force_ctas = 2;
+  g.force_bn = 128;
+  if (int rc = gemm_sm100_launch(g, st)) return (void)cuda_status(static_cast<cudaError_t>(rc), "gate screen gemm");
+  ::fsmoe::count_launch();
+  const double u2 = 0x1.0p-22;  // up to two fp32 ulps per tensor-core addition
+  const double gamp = M * u2 / (1.0 - M * u2);
+  const double cB = gamp * (1.0 + 0x1.0p-8) * 1.01 + 0x1.0p-18 + (M + 2.0) * 0x1.0p-53;
+  const double gam = M * 0x1.0p-24 / (1.0 - M * 0x1.0p-24);  // fp32 |x|^2 sums
+  const auto* xb = static_cast<const __nv_bfloat16*>(x);
+  screen_tc_kernel<KIND, E_MAX><<<(T + ST_TOK - 1) / ST_TOK, ST_MAIN + 32, 0, st>>>(
+      xb, T, M, E, k, P, wn, cB, gam, d.seed, noise_ws, scores_out, spread_out, mask);
+  ::fsmoe::count_launch();
+  constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
+  static DeviceOnce xattr;
+  once_on_device(xattr, [&] { cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM); });
+  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, XSMEM, st>>>(
+      xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
+      spread_out);
+  ::fsmoe::count_launch();
+}
+
 struct PruneWs {
+  __nv_bfloat16* Wtc;  // tensor-core screen: B operand [TC_COLS][M] (hi | lo | 0)
+  float* P;            // its fp32 products [T][TC_COLS]
   float* W32;
   double* WT;
   double* wn;
@@ -1233,6 +1406,8 @@ PruneWs carve(const fsmoe_gate_desc& d, void* base) {
   w.counts = reinterpret_cast<int*>(take(4 * E));
   w.s_exact = reinterpret_cast<double*>(take(8 * T * E));
   w.sp_exact = reinterpret_cast<double*>(take(8 * T * E));
+  w.Wtc = reinterpret_cast<__nv_bfloat16*>(take(2 * TC_COLS * M));
+  w.P = reinterpret_cast<float*>(take(4 * TC_COLS * T));
   w.bytes = off;
   return w;
 }
@@ -1255,10 +1430,25 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
   const int NC = noisy ? 2 * E : E;
   PruneWs w = carve(d, ws);
   FSMOE_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int) * E, st), "gate memset");
-  w_prep_kernel<<<NC, 256, 0, st>>>(M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn);
-  ::fsmoe::count_launch();
   const bool fused = d.x_dtype == FSMOE_BF16 && E <= 32 && NC % 4 == 0 && M % SC_JC == 0 &&
                      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && !getenv("FSMOE_GATE_UNFUSED");
+  // the approximate scores on the tensor cores (tcgen05 GEMM of x against the
+  // bf16 hi / lo split of W); FSMOE_GATE_SIMT keeps the fp32 FFMA2 screen
+  const bool tc = fused && 2 * NC <= TC_COLS && !getenv("FSMOE_GATE_SIMT");
+  if (tc) FSMOE_CUDA_TRY(cudaMemsetAsync(w.Wtc, 0, 2ull * TC_COLS * M, st), "gate memset");
+  w_prep_kernel<<<NC, 256, 0, st>>>(M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn,
+                                    tc ? w.Wtc : nullptr);
+  ::fsmoe::count_launch();
+  if (tc) {
+    double* nz = noise_out ? noise_out : w.noise;
+    if (noisy) {
+      if (E <= 16) launch_fused_tc<0, 16>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+      else launch_fused_tc<0, 32>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+    } else {
+      launch_fused_tc<1, 32>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+    }
+    return cuda_status(cudaGetLastError(), "fsmoe_gate(fused-tc)");
+  }
   if (fused) {
     // the fused screen sums each token's FMA chain without splits: the same
     // bound with the split term kept (conservative)

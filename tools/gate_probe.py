@@ -15,9 +15,12 @@ def run(T=16384, M=1024, E=16, k=1, kind="noisy_topk", reps=5):
     ws = ((torch.rand(M, E, device="cuda", generator=g, dtype=torch.float64) * 2 - 1) / M ** 0.5)
     wn = ((torch.rand(M, E, device="cuda", generator=g, dtype=torch.float64) * 2 - 1) / M ** 0.5)
     out = {}
-    for path in ("pruned", "unfused", "exhaustive"):
+    for path in ("pruned", "simt", "unfused", "exhaustive"):
         os.environ.pop("FSMOE_GATE_EXHAUSTIVE", None)
         os.environ.pop("FSMOE_GATE_UNFUSED", None)
+        os.environ.pop("FSMOE_GATE_SIMT", None)
+        if path == "simt":
+            os.environ["FSMOE_GATE_SIMT"] = "1"
         if path == "exhaustive":
             os.environ["FSMOE_GATE_EXHAUSTIVE"] = "1"
         if path == "unfused":
@@ -33,7 +36,7 @@ def run(T=16384, M=1024, E=16, k=1, kind="noisy_topk", reps=5):
         out[path] = (s.elapsed_time(e) / reps * 1e3, r)
         print(f"{path}: {out[path][0]:.1f} us per gate call")
     a = out["pruned"][1]
-    for other in ("unfused", "exhaustive"):
+    for other in ("simt", "unfused", "exhaustive"):
         b = out[other][1]
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
         print(f"pruned vs {other}: identical picks; max weight diff",
@@ -43,4 +46,8 @@ def run(T=16384, M=1024, E=16, k=1, kind="noisy_topk", reps=5):
 
 
 if __name__ == "__main__":
-    run(reps=int(sys.argv[1]) if len(sys.argv) > 1 else 5)
+    reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+    print("configs[1] shape: T 16384, M 1024, E 16, top-1")
+    run(reps=reps)
+    print("configs[2] shape: T 32768, M 4096, E 8, top-2")
+    run(T=32768, M=4096, E=8, k=2, reps=reps)
