@@ -14,7 +14,8 @@ windows:
 
 What no window absorbs is synchronised after the last layer (the tail).
 
-With `dense=True` every layer has a dense block in front of its MoE layer:
+With `dense=True` every layer has a dense block after its MoE layer (so its
+backward runs first, as in the reference's backward model):
 a chain of bf16 M x M projections (4 M^2 parameters, derive_volumes'
 dense gradient, workload.cpp:53-79) run through torch / cuBLAS — it stands
 for the attention block the framework does not own. Its measured backward
@@ -74,17 +75,21 @@ def _parse_plan(out, n):
 
 
 def slot_loads(plan_layers, n_grad: int, n_layers: int):
-    """Integer elements each backward position synchronises in its MoE window
-    (n_first_moe + x_g) and its dense window (n_first_dense), by rounding the
-    plan's cumulative (conserved) counts; availability is checked: position i
-    may only sync gradient produced by positions < i. Returns (moe loads,
-    dense loads, tail)."""
+    """Integer elements each backward position synchronises in its dense
+    window (n_first_dense) and its MoE window (n_first_moe + x_g), by
+    rounding the plan's cumulative (conserved) counts. Availability follows
+    the reference's backward model (build_backward_model_dag: a layer's dense
+    compute, which produces its gradient, precedes its MoE stage): the dense
+    window of position i syncs only gradient of positions < i (step 1), the
+    MoE window also position i's own (step 2's repair allows origins <= i).
+    Returns (moe loads, dense loads, tail)."""
     cum, prev = 0.0, 0
     moe, dense = [], []
     for i, a in enumerate(plan_layers):
-        for part, out in ((a["n_first_moe"] + a["x_g"], moe), (a["n_first_dense"], dense)):
+        for part, out, avail in ((a["n_first_dense"], dense, i * n_grad),
+                                 (a["n_first_moe"] + a["x_g"], moe, (i + 1) * n_grad)):
             cum += part
-            c = min(int(round(cum)), i * n_grad)  # availability (plan guarantees it up to rounding)
+            c = min(int(round(cum)), avail)  # (the plan guarantees it up to rounding)
             out.append(max(c - prev, 0))
             prev = max(prev, c)
     tail = n_layers * n_grad - prev
@@ -94,9 +99,9 @@ def slot_loads(plan_layers, n_grad: int, n_layers: int):
 class MoEStack:
     """n_layers identical MoE layers (own weights) on this rank's GPU, EP over
     `ep`; `plan_profile` = a fitted profile (plan.fit_profile) or None to
-    profile this box (autotune.collect). `dense=True` puts a DenseBlock in
-    front of every MoE layer and uses its measured backward time as the
-    plan's dense window."""
+    profile this box (autotune.collect). `dense=True` puts a DenseBlock after
+    every MoE layer and uses its measured backward time as the plan's dense
+    window."""
 
     def __init__(self, cfg: MoEConfig, n_layers: int, ep=None, n_grad: int | None = None,
                  plan_profile=None, sync="plan", de=(0, 200, 0.8, 0.9, 1), dense=False,
@@ -161,11 +166,14 @@ class MoEStack:
         return s.elapsed_time(e) / reps
 
     def forward(self, x):
+        # block i: MoE layer, then its dense block — so the backward runs the
+        # dense block first (producing the block's gradient) and the MoE stage
+        # after it, the reference's per-layer backward order
         self._acts = [x]
         for i, l in enumerate(self.layers):
+            x = l.forward(x)
             if self.dense:
                 x = self.dense[i].forward(x)
-            x = l.forward(x)
             self._acts.append(x)
         return x
 
@@ -176,18 +184,12 @@ class MoEStack:
         ptr = 0
         cur = torch.cuda.current_stream()
         for j, l in enumerate(reversed(self.layers)):
-            n = self.loads[j]
-            if n > 0:
-                # this layer's MoE window syncs pool[ptr, ptr + n): gradient of layers < j
-                l.dense_grad = self.pool[ptr: ptr + n]
-                l.bind()
-            dy = l.backward(dy)
-            ptr += n
             own = self.pool[j * self.n_grad: (j + 1) * self.n_grad]
             if self.dense:
                 nd = self.dense_loads[j]
                 if nd > 0 and self.world > 1:
-                    # dense window: pre-sync older gradient beside the dense backward
+                    # dense window: pre-sync older gradient (positions < j)
+                    # beside this position's dense backward
                     self.comm.wait_stream(cur)
                     with torch.cuda.stream(self.comm):
                         self.ep.allreduce(self.pool[ptr: ptr + nd])
@@ -195,6 +197,14 @@ class MoEStack:
                 dy = self.dense[self.L - 1 - j].backward(dy, own)
             elif produce is not None:
                 produce(j, own)
+            n = self.loads[j]
+            if n > 0:
+                # MoE window: pool[ptr, ptr + n) (positions <= j), inside the
+                # MoE backward between its last dispatch and first combine
+                l.dense_grad = self.pool[ptr: ptr + n]
+                l.bind()
+            dy = l.backward(dy)
+            ptr += n
         cur.wait_stream(self.comm)
         if self.world > 1 and self.tail > 0 and ptr < self.pool.numel():
             # the tail, over the layers' own EP communicator (libfsmoe.so)
