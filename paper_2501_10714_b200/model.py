@@ -195,6 +195,10 @@ class MoEStack:
                         self.ep.allreduce(self.pool[ptr: ptr + nd])
                 ptr += nd
                 dy = self.dense[self.L - 1 - j].backward(dy, own)
+                # the pre-sync rides beside the dense backward only: it must be
+                # done before the MoE backward issues its own collectives on
+                # the same communicator (one NCCL op at a time, in issue order)
+                cur.wait_stream(self.comm)
             elif produce is not None:
                 produce(j, own)
             n = self.loads[j]
