@@ -8,3 +8,5 @@ for k in screen_tc_kernel exact_final_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:$k -c 4 -o $O/$k -f python tools/gate_probe.py 1 > $O/ncu_$k.log 2>&1
   echo "$k rc=$?"
 done
+ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -c 1 -o $O/screen_gemm -f python tools/gate_probe.py 1 > $O/ncu_screen_gemm.log 2>&1
+echo "screen_gemm rc=$?"
