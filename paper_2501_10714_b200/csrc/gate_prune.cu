@@ -886,16 +886,28 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
     const int tl = tid >> 2, q = tid & 3;
     float nacc = 0.f;
     if (tl < ntok) {
+      // batches of 8 independent 16-byte loads in flight per thread (the
+      // loop is load-latency bound: one load per iteration stalled ~40 % of
+      // the kernel's samples on its result)
       const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<long long>(t0 + tl) * M);
       const int nv = M / 8;
-      for (int v = q; v < nv; v += 4) {
-        const uint4 u = xr[v];
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+      constexpr int NB = 8;
+      for (int v0 = q; v0 < nv; v0 += 4 * NB) {
+        uint4 u[NB];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float a = __uint_as_float(w4[c] << 16), b = __uint_as_float(w4[c] & 0xffff0000u);
-          nacc = fmaf(a, a, nacc);
-          nacc = fmaf(b, b, nacc);
+        for (int i = 0; i < NB; ++i) {
+          const int v = v0 + 4 * i;
+          u[i] = v < nv ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const uint32_t w4[4] = {u[i].x, u[i].y, u[i].z, u[i].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float a = __uint_as_float(w4[c] << 16), b = __uint_as_float(w4[c] & 0xffff0000u);
+            nacc = fmaf(a, a, nacc);
+            nacc = fmaf(b, b, nacc);
+          }
         }
       }
     }
@@ -965,13 +977,17 @@ struct XfSmem {
   static constexpr int XS = XF_TOK * XF_XROW;             // token rows of one stage
   static constexpr int WS = NPROJ * E_MAX * XF_WROW * 8;   // W^T rows (fp64) of one stage
   static constexpr int STAGE = XS + WS;
-  static constexpr int BYTES = 2 * STAGE;
+  static constexpr int NS = 3;                               // stages in flight
+  static constexpr int BYTES = NS * STAGE;                   // at E = E_MAX
+  // the launched stage stride holds the W^T rows of the E actual experts
+  static __host__ __device__ int stride(int E) { return XS + NPROJ * E * XF_WROW * 8; }
 };
 
 // Exact fp64 logits of each token's candidates (the reference's sequential
 // separately rounded mul/add over j, workload.cpp:103-108) with the token
 // rows and all W^T rows streamed through shared memory in XF_JC-column
-// stages (cp.async, double-buffered); thread = (token, candidate, projection).
+// stages (cp.async, S::NS stages in flight); thread = (token, candidate,
+// projection).
 // Then the final exact top-k, weights and picks for the block's tokens.
 template <int KIND, int E_MAX>
 __global__ void __launch_bounds__(XF_THREADS)
@@ -992,9 +1008,10 @@ __global__ void __launch_bounds__(XF_THREADS)
   const int t0 = blockIdx.x * XF_TOK;
   const int ntok = min(XF_TOK, T - t0);
   const int nW = NPROJ * E;
+  const int stg = S::stride(E);
   auto issue = [&](int ck) {
     if (ck * XF_JC < M) {
-      uint8_t* st = sm + (ck & 1) * S::STAGE;
+      uint8_t* st = sm + (ck % S::NS) * stg;
       const int j0 = ck * XF_JC;
       for (int i = tid; i < XF_TOK * (XF_JC / 8); i += XF_THREADS) {
         const int r = i / (XF_JC / 8), c = i % (XF_JC / 8);
@@ -1134,101 +1151,116 @@ __global__ void __launch_bounds__(XF_THREADS)
   }
   __syncthreads();
   const int nc = nitems;
-  const int nwork = nc * NPROJ;
-  // work item = (projection, candidate), projection-major so that the lanes of
-  // a warp read rows of one projection (padded rows: conflict-free); a thread
-  // holds up to 2 dot products (a block rarely has > 256 items)
-  double acc0 = 0.0, acc1 = 0.0;
+  // work item = candidate (token, expert); its NPROJ chains (score and noise
+  // projection) share every x load and its fp64 conversion -- the
+  // conversions (F2F, XU pipe) bounded the kernel when each projection
+  // converted the row again. A thread holds up to 2 items (a block rarely
+  // has > 2 * XF_THREADS candidates; the rest run from global memory below).
+  const int nwork = nc;
+  double acc0[NPROJ], acc1[NPROJ];
+#pragma unroll
+  for (int pj = 0; pj < NPROJ; ++pj) acc0[pj] = acc1[pj] = 0.0;
   const int it0 = tid, it1 = tid + XF_THREADS;
-  short2 te0 = make_short2(0, 0), te1 = make_short2(0, 0);
-  int pj0 = 0, pj1 = 0;
-  if (it0 < nwork) { te0 = items[it0 % nc]; pj0 = it0 / nc; }
-  if (it1 < nwork) { te1 = items[it1 % nc]; pj1 = it1 / nc; }
-  // A block with only a handful of dot products (the few tokens whose bound
+  const short2 te0 = it0 < nwork ? items[it0] : make_short2(0, 0);
+  const short2 te1 = it1 < nwork ? items[it1] : make_short2(0, 0);
+  // 8 consecutive terms of every chain: acc_p = acc_p + x_j * W_p[j], in j
+  // order, each product and sum separately rounded (workload.cpp:103-108)
+  auto chain8 = [&](double (&acc)[NPROJ], const uint4 u, const double* const (&wr)[NPROJ]) {
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double xa = static_cast<double>(__uint_as_float(w4[q] << 16));
+      const double xb = static_cast<double>(__uint_as_float(w4[q] & 0xffff0000u));
+#pragma unroll
+      for (int pj = 0; pj < NPROJ; ++pj) {
+        const double2 wv = *reinterpret_cast<const double2*>(wr[pj] + 2 * q);
+        acc[pj] = __dadd_rn(acc[pj], __dmul_rn(xa, wv.x));
+        acc[pj] = __dadd_rn(acc[pj], __dmul_rn(xb, wv.y));
+      }
+    }
+  };
+  // A block with only a handful of candidates (the few tokens whose bound
   // leaves 2+ candidates) bulk-loads just those rows and runs each chain from
   // shared memory with no per-chunk barriers: the chain's latency, not the
   // staging pipeline, is then the block's time.
   __shared__ __align__(8) uint64_t sbar;
-  const long long small_bytes = static_cast<long long>(nwork) * M * 10;
-  const bool small = nwork > 0 && small_bytes <= S::BYTES && M % 8 == 0;
+  const long long item_bytes = static_cast<long long>(M) * (2 + 8 * NPROJ);
+  const long long small_bytes = static_cast<long long>(nwork) * item_bytes;
+  const bool small = nwork > 0 && small_bytes <= S::NS * stg && M % 8 == 0;
   if (small) {
     if (tid == 0) {
       fsmoe_dev::mbar_init(&sbar, 1);
       fsmoe_dev::fence_barrier_init();
       fsmoe_dev::mbar_arrive_expect_tx(&sbar, static_cast<uint32_t>(small_bytes));
       for (int it = 0; it < nwork; ++it) {
-        const short2 te = items[it % nc];
-        const int pj = it / nc;
-        uint8_t* d = sm + static_cast<long long>(it) * M * 10;
+        const short2 te = items[it];
+        uint8_t* d = sm + static_cast<long long>(it) * item_bytes;
         fsmoe_dev::bulk_load(d, x + static_cast<long long>(t0 + te.x) * M, static_cast<uint32_t>(M * 2), &sbar);
-        fsmoe_dev::bulk_load(d + M * 2, WT + static_cast<long long>(pj * E + te.y) * M,
-                             static_cast<uint32_t>(M * 8), &sbar);
+        for (int pj = 0; pj < NPROJ; ++pj)
+          fsmoe_dev::bulk_load(d + M * 2 + static_cast<long long>(pj) * M * 8,
+                               WT + static_cast<long long>(pj * E + te.y) * M, static_cast<uint32_t>(M * 8), &sbar);
       }
     }
     __syncthreads();
     if (tid < nwork) {
       fsmoe_dev::mbar_wait(&sbar, 0);
-      const uint8_t* xr = sm + static_cast<long long>(tid) * M * 10;
-      const double* wr = reinterpret_cast<const double*>(xr + M * 2);
-      double acc = 0.0;
-#pragma unroll 4
+      const uint8_t* xr = sm + static_cast<long long>(tid) * item_bytes;
+      const double* w0 = reinterpret_cast<const double*>(xr + M * 2);
+#pragma unroll 2
       for (int j = 0; j < M; j += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(xr + 2 * j);
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        const double* wr[NPROJ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 wv = *reinterpret_cast<const double2*>(wr + j + 2 * q);
-          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] << 16)), wv.x));
-          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] & 0xffff0000u)), wv.y));
-        }
+        for (int pj = 0; pj < NPROJ; ++pj) wr[pj] = w0 + static_cast<long long>(pj) * M + j;
+        chain8(acc0, *reinterpret_cast<const uint4*>(xr + 2 * j), wr);
       }
-      ex[pj0][te0.x][te0.y] = acc;
+#pragma unroll
+      for (int pj = 0; pj < NPROJ; ++pj) ex[pj][te0.x][te0.y] = acc0[pj];
     }
   }
   // otherwise stream the token / weight rows in chunks (when there is work)
   const int nck = (nwork > 0 && !small) ? (M + XF_JC - 1) / XF_JC : 0;
-  if (nck > 0) {
-    issue(0);
-    issue(1);
-  }
+  if (nck > 0)
+    for (int i = 0; i < S::NS - 1; ++i) issue(i);  // every issue commits a group (maybe empty)
   for (int ck = 0; ck < nck; ++ck) {
-    if (ck + 1 < nck) cp_async_wait<1>();
-    else cp_async_wait<0>();
+    cp_async_wait<S::NS - 2>();  // chunk ck has landed
     __syncthreads();
-    const uint8_t* st = sm + (ck & 1) * S::STAGE;
+    const uint8_t* st = sm + (ck % S::NS) * stg;
     const double* ws = reinterpret_cast<const double*>(st + S::XS);
-    auto run = [&](double& acc, short2 te, int pj) {
+    auto run = [&](double (&acc)[NPROJ], short2 te) {
       const uint8_t* xr = st + te.x * XF_XROW;
-      const double* wr = ws + (pj * E + te.y) * XF_WROW;
-#pragma unroll 4
+#pragma unroll 2
       for (int j = 0; j < XF_JC; j += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(xr + 2 * j);
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        const double* wr[NPROJ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 wv = *reinterpret_cast<const double2*>(wr + j + 2 * q);
-          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] << 16)), wv.x));
-          acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__uint_as_float(w4[q] & 0xffff0000u)), wv.y));
-        }
+        for (int pj = 0; pj < NPROJ; ++pj) wr[pj] = ws + (pj * E + te.y) * XF_WROW + j;
+        chain8(acc, *reinterpret_cast<const uint4*>(xr + 2 * j), wr);
       }
     };
-    if (it0 < nwork) run(acc0, te0, pj0);
-    if (it1 < nwork) run(acc1, te1, pj1);
+    if (it0 < nwork) run(acc0, te0);
+    if (it1 < nwork) run(acc1, te1);
     __syncthreads();
-    issue(ck + 2);
+    issue(ck + S::NS - 1);
   }
-  if (!small && it0 < nwork) ex[pj0][te0.x][te0.y] = acc0;
-  if (!small && it1 < nwork) ex[pj1][te1.x][te1.y] = acc1;
-  // more than 2 * XF_THREADS dot products: the rest from global memory
+#pragma unroll
+  for (int pj = 0; pj < NPROJ; ++pj) {
+    if (!small && it0 < nwork) ex[pj][te0.x][te0.y] = acc0[pj];
+    if (!small && it1 < nwork) ex[pj][te1.x][te1.y] = acc1[pj];
+  }
+  // more than 2 * XF_THREADS candidates: the rest from global memory
   for (int it = it1 + XF_THREADS; it < nwork; it += XF_THREADS) {
-    const short2 te = items[it % nc];
-    const int pj = it / nc;
+    const short2 te = items[it];
     const __nv_bfloat16* xr = x + static_cast<long long>(t0 + te.x) * M;
-    const double* wr = WT + static_cast<long long>(pj * E + te.y) * M;
-    double acc = 0.0;
-    for (int j = 0; j < M; ++j)
-      acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__bfloat162float(xr[j])), wr[j]));
-    ex[pj][te.x][te.y] = acc;
+    double acc[NPROJ];
+#pragma unroll
+    for (int pj = 0; pj < NPROJ; ++pj) acc[pj] = 0.0;
+    for (int j = 0; j < M; ++j) {
+      const double xv = static_cast<double>(__bfloat162float(xr[j]));
+#pragma unroll
+      for (int pj = 0; pj < NPROJ; ++pj)
+        acc[pj] = __dadd_rn(acc[pj], __dmul_rn(xv, WT[static_cast<long long>(pj * E + te.y) * M + j]));
+    }
+#pragma unroll
+    for (int pj = 0; pj < NPROJ; ++pj) ex[pj][te.x][te.y] = acc[pj];
   }
   __syncthreads();
   if (tid >= ntok) return;
@@ -1312,7 +1344,10 @@ void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const floa
   constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
   static DeviceOnce xattr;
   once_on_device(xattr, [&] { cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM); });
-  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, XSMEM, st>>>(
+  // E's stages (at least the certain-pick path's dot / bound scratch)
+  const int xs_rt = std::max(XfSmem<KIND == 0 ? 2 : 1, E_MAX>::NS * XfSmem<KIND == 0 ? 2 : 1, E_MAX>::stride(E),
+                             XF_TOK * E_MAX * 2 * 8 * 2);
+  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st>>>(
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
       spread_out);
   ::fsmoe::count_launch();
@@ -1351,7 +1386,10 @@ void launch_fused_tc(const fsmoe_gate_desc& d, const void* x, const __nv_bfloat1
   constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
   static DeviceOnce xattr;
   once_on_device(xattr, [&] { cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM); });
-  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, XSMEM, st>>>(
+  // E's stages (at least the certain-pick path's dot / bound scratch)
+  const int xs_rt = std::max(XfSmem<KIND == 0 ? 2 : 1, E_MAX>::NS * XfSmem<KIND == 0 ? 2 : 1, E_MAX>::stride(E),
+                             XF_TOK * E_MAX * 2 * 8 * 2);
+  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st>>>(
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
       spread_out);
   ::fsmoe::count_launch();

@@ -7,6 +7,9 @@ evict_last, 128 = B loads evict_first), one launch each, meant to run under
         --log-file gpurun_out/l2hint.csv python tools/l2hint_probe.py
 
 and summarised with `python tools/l2hint_probe.py --summarise gpurun_out/l2hint.csv`.
+The hint flags were removed from the kernel after this experiment (no
+measurable gain, profiles/r02_gemm_experiments.md); the probe is kept as the
+record of how it was measured.
 """
 import csv
 import json
