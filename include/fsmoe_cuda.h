@@ -269,7 +269,8 @@ typedef struct fsmoe_gemm_desc {
   const void* A;
   const void* B;
   const long long* valid_rows; /* optional, per block */
-  int epi;         /* 0 store bf16, 1 store f32, 2 gelu fwd, 3 swiglu fwd, 4 gelu bwd, 5 swiglu bwd.
+  int epi;         /* 0 store bf16, 1 store f32, 2 gelu fwd, 3 swiglu fwd, 4 gelu bwd, 5 swiglu bwd,
+                    * 6 add bf16 (row-grouped, tcgen05 only: D = bf16(acc + Zin), Zin may be D).
                     * bf16 gelu: fwd writes D = gelu'(Z) (what the backward
                     * needs, so it does no transcendental work) and D2 = gelu(Z);
                     * bwd writes D = acc * Zin with Zin that saved gelu'(Z). */

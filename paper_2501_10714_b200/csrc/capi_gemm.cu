@@ -132,7 +132,7 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   p.ldd2 = d->ldd2;
   p.ldz = d->ldz;
   p.accumulate = d->accumulate != 0;
-  if (d->epi < 0 || d->epi > 5) return config_error("gemm: unknown epilogue");
+  if (d->epi < 0 || d->epi > 6) return config_error("gemm: unknown epilogue");
   p.max_sms = d->max_sms;
   p.force_ctas = d->force_ctas;
   p.force_bn = d->force_bn;

@@ -13,6 +13,7 @@
 #include <type_traits>
 
 #include "capi_common.h"
+#include "gemm.h"
 #include "host_once.h"
 #include "kernels.h"
 #include "route_common.cuh"
@@ -624,6 +625,173 @@ void dx_acc(int xdt, int T, int M, int NC, const double* G, long long gst, long 
   }
 }
 
+// ------------------------------------------------ tensor-core forms --
+// For bf16 tokens the two contractions of a noisy / sigmoid gate backward
+// run on the tcgen05 grouped GEMM (they were fp32 SIMT FMA bound: 2 T M NC2
+// flops each, ~0.2 of HBM at the configs[2] shape):
+//   x^T [G1 | G2]: a k-grouped GEMM of x against G split into three bf16
+//     terms (hi, mid, lo: ~24 significant bits, fp32 accumulation, exact
+//     products) over S token blocks -> fp32 partials, then a fixed-order fp64
+//     sum of blocks and terms;
+//   dx += [G1 | G2] [W1 | W2]^T: a row-grouped GEMM of K = 3 NC2 (G_hi W_hi +
+//     G_hi W_lo + G_lo W_hi, ~16 bits) with the AddBF16 epilogue adding into
+//     dx in place (bf16(dx + acc), the rounding of the SIMT form).
+constexpr int TC_KMAX = 128;  // 3 * NC2 rounded up to 64 columns
+
+__device__ __forceinline__ double gval(int c, int NC, long long t, const double* G1, const double* G2,
+                                       long long gst, long long gsc) {
+  return c < NC ? G1[t * gst + c * gsc] : G2[t * gst + (c - NC) * gsc];
+}
+
+// Gx[t][No] = [hi | mid | lo | 0] of G's NC2 columns; Gd[t][Kp] = [hi | hi | lo' | 0]
+// (lo' = bf16(g - hi), the two-term split)
+__global__ void g_split_kernel(int T, int NC, int NC2, int No, int Kp, const double* __restrict__ G1,
+                               const double* __restrict__ G2, long long gst, long long gsc,
+                               __nv_bfloat16* __restrict__ Gx, __nv_bfloat16* __restrict__ Gd) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int W = No > Kp ? No : Kp;
+  if (i >= static_cast<long long>(T) * W) return;
+  const long long t = i / W;
+  const int col = static_cast<int>(i % W);
+  const int c = col % NC2, term = col / NC2;
+  double g = 0.0;
+  if (term < 3) g = gval(c, NC, t, G1, G2, gst, gsc);
+  const __nv_bfloat16 hi = __double2bfloat16(g);
+  const double r1 = g - static_cast<double>(__bfloat162float(hi));
+  const __nv_bfloat16 mid = __double2bfloat16(r1);
+  const __nv_bfloat16 lo = __double2bfloat16(r1 - static_cast<double>(__bfloat162float(mid)));
+  const __nv_bfloat16 z = __float2bfloat16(0.f);
+  if (col < No) Gx[t * No + col] = term == 0 ? hi : term == 1 ? mid : term == 2 ? lo : z;
+  if (col < Kp) Gd[t * Kp + col] = term == 0 || term == 1 ? hi : term == 2 ? mid : z;
+}
+
+// Wd[j][Kp] = [W_hi | W_lo | W_hi | 0] over the NC2 columns of [W1 | W2]
+__global__ void w_split_kernel(int M, int NC, int NC2, int Kp, const double* __restrict__ W1,
+                               const double* __restrict__ W2, long long wsj, long long wsc,
+                               __nv_bfloat16* __restrict__ Wd) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(M) * Kp) return;
+  const long long j = i / Kp;
+  const int col = static_cast<int>(i % Kp);
+  const int c = col % NC2, term = col / NC2;
+  double w = 0.0;
+  if (term < 3) w = c < NC ? W1[j * wsj + c * wsc] : W2[j * wsj + (c - NC) * wsc];
+  const __nv_bfloat16 hi = __double2bfloat16(w);
+  const __nv_bfloat16 lo = __double2bfloat16(w - static_cast<double>(__bfloat162float(hi)));
+  Wd[i] = term == 0 || term == 2 ? hi : term == 1 ? lo : __float2bfloat16(0.f);
+}
+
+// out1 / out2 [j][c] (+)= sum_s (P[s][j][c] + P[s][j][NC2 + c] + P[s][j][2 NC2 + c]), fixed order
+__global__ void xtg_tc_reduce_kernel(int S, int M, int NC, int NC2, int No, const float* __restrict__ P,
+                                     double* __restrict__ out1, double* __restrict__ out2, long long osj,
+                                     long long osc, int accumulate) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(M) * NC2) return;
+  const int j = static_cast<int>(i / NC2), c = static_cast<int>(i % NC2);
+  double a = 0.0;
+  for (int s = 0; s < S; ++s) {
+    const float* r = P + (static_cast<long long>(s) * M + j) * No;
+    a += static_cast<double>(r[c]);
+    a += static_cast<double>(r[NC2 + c]);
+    a += static_cast<double>(r[2 * NC2 + c]);
+  }
+  double* o = c < NC ? out1 + j * osj + c * osc : out2 + j * osj + (c - NC) * osc;
+  *o = accumulate ? *o + a : a;
+}
+
+struct TcShape {
+  int NC2, No, Kp, S;
+};
+// the tensor-core forms apply: bf16 tokens, 64-aligned model dim, <= 42 columns
+bool tc_shape(int xdt, int T, int M, int NC2, TcShape* sh) {
+  if (xdt != FSMOE_BF16 || M % 64 || NC2 <= 0 || 3 * NC2 > TC_KMAX || T < 64) return false;
+  sh->NC2 = NC2;
+  sh->No = sh->Kp = (3 * NC2 + 63) / 64 * 64;
+  // token blocks of the x^T G GEMM: about two pair tiles per SM, T divisible
+  const int mt = (M + 255) / 256;
+  int S = (device_sms() + mt - 1) / mt;
+  if (S > 64) S = 64;
+  while (S > 1 && (T % S || T / S < 64)) --S;
+  sh->S = S;
+  return true;
+}
+size_t tc_ws_elems(int T, int M, int NC2max) {  // in doubles (8-byte units)
+  TcShape sh{};
+  if (!tc_shape(FSMOE_BF16, T, M, NC2max, &sh)) return 0;
+  const size_t b = static_cast<size_t>(T) * sh.No * 2 + static_cast<size_t>(T) * sh.Kp * 2 +
+                   static_cast<size_t>(M) * sh.Kp * 2 + static_cast<size_t>(sh.S) * M * sh.No * 4;
+  return (b + 7) / 8 + 128;
+}
+
+// x^T [G1 | G2] and dx += [G1 | G2] [W1 | W2]^T on the tensor cores.
+// Returns -1 when the shape needs the SIMT kernels (nothing was written),
+// else a status. tw: workspace of tc_ws_elems.
+int gate_bwd_tc(int xdt, int T, int M, int NC, const void* X, const double* G1, const double* G2,
+                 long long gst, long long gsc, double* out1, double* out2, long long osj, long long osc,
+                 const double* W1, const double* W2, long long wsj, long long wsc, void* dx, double* tw,
+                 cudaStream_t st) {
+  const int NC2 = G2 ? 2 * NC : NC;
+  TcShape sh{};
+  if (!tw || !tc_shape(xdt, T, M, NC2, &sh)) return -1;
+  char* p = reinterpret_cast<char*>(tw);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  auto* Gx = reinterpret_cast<__nv_bfloat16*>(take(static_cast<size_t>(T) * sh.No * 2));
+  auto* Gd = reinterpret_cast<__nv_bfloat16*>(take(static_cast<size_t>(T) * sh.Kp * 2));
+  auto* Wd = reinterpret_cast<__nv_bfloat16*>(take(static_cast<size_t>(M) * sh.Kp * 2));
+  auto* P = reinterpret_cast<float*>(take(static_cast<size_t>(sh.S) * M * sh.No * 4));
+  const long long ng = static_cast<long long>(T) * (sh.No > sh.Kp ? sh.No : sh.Kp);
+  g_split_kernel<<<static_cast<int>((ng + 255) / 256), 256, 0, st>>>(T, NC, NC2, sh.No, sh.Kp, G1, G2 ? G2 : G1,
+                                                                     gst, gsc, Gx, Gd);
+  ::fsmoe::count_launch();
+  const long long nw = static_cast<long long>(M) * sh.Kp;
+  w_split_kernel<<<static_cast<int>((nw + 255) / 256), 256, 0, st>>>(M, NC, NC2, sh.Kp, W1, W2 ? W2 : W1, wsj,
+                                                                     wsc, Wd);
+  ::fsmoe::count_launch();
+  // x^T G: S blocks of T/S tokens, each its own output block (n_w = S)
+  GemmProblem g{};
+  g.kind = GemmKind::KGrouped;
+  g.nblk = sh.S;
+  g.n_w = sh.S;
+  g.rows = g.rows_total = T / sh.S;
+  g.Mo = M;
+  g.No = sh.No;
+  g.A = X;
+  g.B = Gx;
+  g.epi = Epi::StoreF32;
+  g.D = P;
+  g.ldd = sh.No;
+  g.force_ctas = 2;
+  g.force_bn = 128;
+  int rc = gemm_sm100_launch(g, st);
+  if (rc != cudaSuccess) return cuda_status(static_cast<cudaError_t>(rc), "gate backward x^T G (tcgen05)");
+  const long long nr = static_cast<long long>(M) * NC2;
+  xtg_tc_reduce_kernel<<<static_cast<int>((nr + 255) / 256), 256, 0, st>>>(sh.S, M, NC, NC2, sh.No, P, out1,
+                                                                           out2 ? out2 : out1, osj, osc, 1);
+  ::fsmoe::count_launch();
+  // dx += Gd . Wd^T, in place through the AddBF16 epilogue
+  GemmProblem h{};
+  h.kind = GemmKind::RowGrouped;
+  h.nblk = 1;
+  h.n_w = 1;
+  h.rows = h.rows_total = T;
+  h.K = sh.Kp;
+  h.N = M;
+  h.A = Gd;
+  h.B = Wd;
+  h.epi = Epi::AddBF16;
+  h.D = dx;
+  h.ldd = M;
+  h.Zin = dx;
+  h.ldz = M;
+  rc = gemm_sm100_launch(h, st);
+  if (rc != cudaSuccess) return cuda_status(static_cast<cudaError_t>(rc), "gate backward dx (tcgen05)");
+  return FSMOE_OK;
+}
+
 }  // namespace
 
 // Partial-sum elements the largest x^T G of a gate backward needs: every
@@ -649,9 +817,11 @@ size_t xt_part_elems(int T, int M, int E, int P) {
 size_t gate_bwd_workspace_bytes(const fsmoe_gate_desc& d) {
   const size_t T = d.tokens, E = d.score_cols, M = d.model_dim, P = d.proj_rows > 0 ? d.proj_rows : 0;
   auto r = [](size_t n) { return (n * 8 + 255) & ~size_t(255); };
+  const size_t tcw = d.x_dtype == FSMOE_BF16 ? tc_ws_elems(static_cast<int>(T), static_cast<int>(M),
+                                                            static_cast<int>(2 * E)) : 0;
   return r(T * E) * 2 + r(T * P) * 2 + r(xt_part_elems(static_cast<int>(T), static_cast<int>(M),
                                                         static_cast<int>(E), static_cast<int>(P))) +
-         r(P * E) + r(E) * 2 + 1024;
+         r(P * E) + r(E) * 2 + r(tcw) + 1024;
 }
 
 int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_score,
@@ -670,12 +840,20 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
   double* dS = w.take(static_cast<size_t>(T) * E);
   const int P = d.proj_rows > 0 ? d.proj_rows : 0;
   double* part = w.take(xt_part_elems(T, M, E, P));
+  const size_t tcw = d.x_dtype == FSMOE_BF16 ? tc_ws_elems(T, M, 2 * E) : 0;
+  double* tw = tcw ? w.take(tcw) : nullptr;
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
       dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dZ = w.take(static_cast<size_t>(T) * E);
       long long n = static_cast<long long>(T) * E;
       noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ); ::fsmoe::count_launch();
+      const int tc = gate_bwd_tc(d.x_dtype, T, M, E, x, dS, dZ, E, 1, dWs, dWn, E, 1, w_score, w_noise, E, 1,
+                                 dx, tw, st);
+      if (tc >= 0) {
+        if (tc != FSMOE_OK) return tc;
+        break;
+      }
       if (!xtg_pair(d.x_dtype, T, M, E, x, dS, dZ, E, 1, dWs, dWn, E, 1, 1, part, st)) {
         xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
         xtg(d.x_dtype, T, M, E, x, dZ, E, 1, dWn, E, 1, 1, part, st);
@@ -688,6 +866,12 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
     }
     case FSMOE_GATE_SIGMOID_TOPK: {
       dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(1, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
+      const int tc = gate_bwd_tc(d.x_dtype, T, M, E, x, dS, nullptr, E, 1, dWs, nullptr, E, 1, w_score, nullptr,
+                                 E, 1, dx, tw, st);
+      if (tc >= 0) {
+        if (tc != FSMOE_OK) return tc;
+        break;
+      }
       if (!xtg_pair(d.x_dtype, T, M, E, x, dS, nullptr, E, 1, dWs, nullptr, E, 1, 1, part, st))
         xtg(d.x_dtype, T, M, E, x, dS, E, 1, dWs, E, 1, 1, part, st);
       dx_acc(d.x_dtype, T, M, E, dS, E, 1, w_score, E, 1, dx, st);

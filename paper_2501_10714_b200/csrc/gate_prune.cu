@@ -845,6 +845,7 @@ __global__ void __launch_bounds__(512 + SC_MT_WARPS * 32)
 constexpr int TC_COLS = 128;  // GEMM output columns (2 NC <= 128)
 constexpr int ST_TOK = 32;    // tokens per screen_tc block (4 threads each + one noise-draw warp)
 constexpr int ST_MAIN = 4 * ST_TOK;
+constexpr int ST_TPT = ST_MAIN / ST_TOK;
 
 template <int KIND, int E_MAX>
 __global__ void __launch_bounds__(ST_MAIN + 32)
@@ -854,7 +855,7 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
                      double* __restrict__ scores_out, double* __restrict__ spread_out,
                      uint64_t* __restrict__ mask) {
   __shared__ uint64_t draws[KIND == 0 ? ST_TOK * 2 * E_MAX : 1];
-  __shared__ float nrm[ST_TOK * 4];
+  __shared__ float nrm[ST_MAIN];  // [token][ST_TPT partial sums]
   __shared__ double lo[ST_TOK * E_MAX], hi[ST_TOK * E_MAX];
   const int tid = threadIdx.x;
   const int t0 = blockIdx.x * ST_TOK;
@@ -881,9 +882,11 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
         }
       }
   } else {
-    // |x_t|^2 from the exact squares of the bf16 values: four threads per
-    // token, each a quarter of the row (16-byte loads)
-    const int tl = tid >> 2, q = tid & 3;
+    // |x_t|^2 from the exact squares of the bf16 values: ST_TPT threads per
+    // token, each an interleaved share of the row (16-byte loads). (512-thread
+    // blocks doing every item in one round measured slower: fewer blocks fit
+    // an SM, so the grid no longer ran in a single wave.)
+    const int tl = tid / ST_TPT, q = tid % ST_TPT;
     float nacc = 0.f;
     if (tl < ntok) {
       // batches of 8 independent 16-byte loads in flight per thread (the
@@ -892,11 +895,11 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
       const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<long long>(t0 + tl) * M);
       const int nv = M / 8;
       constexpr int NB = 8;
-      for (int v0 = q; v0 < nv; v0 += 4 * NB) {
+      for (int v0 = q; v0 < nv; v0 += ST_TPT * NB) {
         uint4 u[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const int v = v0 + 4 * i;
+          const int v = v0 + ST_TPT * i;
           u[i] = v < nv ? __ldg(xr + v) : make_uint4(0u, 0u, 0u, 0u);
         }
 #pragma unroll
@@ -917,8 +920,11 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
   for (int pi = tid; pi < ntok * E; pi += blockDim.x) {
     const int tl = pi / E, e = pi % E;
     const long long o = static_cast<long long>(t0 + tl) * E + e;
-    const double xs2 = (static_cast<double>(nrm[4 * tl]) + static_cast<double>(nrm[4 * tl + 1])) +
-                       (static_cast<double>(nrm[4 * tl + 2]) + static_cast<double>(nrm[4 * tl + 3]));
+    // fixed-order fp64 sum of the partials (any order is inside gam's bound;
+    // the 1e-12 slack below covers the fp64 roundings)
+    double xs2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < ST_TPT; ++i) xs2 += static_cast<double>(nrm[tl * ST_TPT + i]);
     const double xnorm = sqrt(xs2 * (1.0 + 2.0 * gam)) * (1.0 + 1e-12);
     const float* pr = P + static_cast<long long>(t0 + tl) * TC_COLS;
     const double r = static_cast<double>(pr[e]) + static_cast<double>(pr[NC + e]);
@@ -1131,23 +1137,22 @@ __global__ void __launch_bounds__(XF_THREADS)
       __syncthreads();
     }
   }
-  if (tid < 32) {  // exclusive scan of the 64 counts by one warp
-    const int c0 = cnt[tid], c1 = cnt[tid + 32];
-    int a0 = c0, a1 = c1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v0 = __shfl_up_sync(0xffffffffu, a0, o), v1 = __shfl_up_sync(0xffffffffu, a1, o);
-      if (tid >= o) { a0 += v0; a1 += v1; }
+  if (tid < 32) {
+    // candidate list in expert-major order (then token): the lanes of a warp
+    // then mostly share one expert, so their W^T reads in the chains below
+    // are shared-memory broadcasts (token-major lists made every lane read
+    // its own row: the kernel was bound by shared-memory wavefronts)
+    const uint64_t m0 = cnt[tid] ? msk[tid] : 0ULL, m1 = cnt[tid + 32] ? msk[tid + 32] : 0ULL;
+    const unsigned lt = (1u << tid) - 1u;
+    int base = 0;
+    for (int e = 0; e < E; ++e) {
+      const bool h0 = (m0 >> e) & 1ULL, h1 = (m1 >> e) & 1ULL;
+      const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
+      if (h0) items[base + __popc(b0 & lt)] = make_short2(static_cast<short>(tid), static_cast<short>(e));
+      if (h1) items[base + __popc(b0) + __popc(b1 & lt)] = make_short2(static_cast<short>(tid + 32), static_cast<short>(e));
+      base += __popc(b0) + __popc(b1);
     }
-    const int tot0 = __shfl_sync(0xffffffffu, a0, 31);
-    int w0 = a0 - c0, w1 = tot0 + a1 - c1;
-    if (c0)
-      for (uint64_t mm = msk[tid]; mm; mm &= mm - 1)
-        items[w0++] = make_short2(static_cast<short>(tid), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
-    if (c1)
-      for (uint64_t mm = msk[tid + 32]; mm; mm &= mm - 1)
-        items[w1++] = make_short2(static_cast<short>(tid + 32), static_cast<short>(__ffsll(static_cast<long long>(mm)) - 1));
-    if (tid == 31) nitems = tot0 + a1;
+    if (tid == 0) nitems = base;
   }
   __syncthreads();
   const int nc = nitems;

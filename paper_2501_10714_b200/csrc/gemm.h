@@ -42,6 +42,7 @@ enum class Epi : int {
   SwigluFwd = 3,   // acc cols interleaved [gate128|up128]: Z = acc, H = silu(g)*u
   GeluBwd = 4,     // acc = dH; dZ = dH * Zin, Zin = the saved gelu'(Z)  N = H
   SwigluBwd = 5,   // acc = dH (N = H); writes dZ at interleaved gate/up columns
+  AddBF16 = 6,     // D = bf16(acc + Zin) (Zin may alias D: in-place accumulation of a bf16 output)
 };
 
 struct GemmProblem {

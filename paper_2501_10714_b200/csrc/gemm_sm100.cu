@@ -466,7 +466,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool tma_epi = p.epi == static_cast<int>(Epi::StoreBF16) ||
                          p.epi == static_cast<int>(Epi::StoreF32) ||
                          p.epi == static_cast<int>(Epi::GeluFwd) ||
-                         p.epi == static_cast<int>(Epi::GeluBwd);
+                         p.epi == static_cast<int>(Epi::GeluBwd) ||
+                         p.epi == static_cast<int>(Epi::AddBF16);
+    // GeluBwd and AddBF16 combine the accumulator with a loaded bf16 box
+    const bool zbox_epi = p.epi == static_cast<int>(Epi::GeluBwd) || p.epi == static_cast<int>(Epi::AddBF16);
     // this lane's row inside a box: unit k of the row lives at (k ^ (lane & 7))
     auto box_row = [&](uint8_t* box) { return reinterpret_cast<uint4*>(box + lane * 128); };
     auto store_box = [&](const CUtensorMap* m, const void* box, int x0, int x1, int x2) {
@@ -502,8 +505,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
       }
-      if (p.epi == static_cast<int>(Epi::GeluBwd)) {
-        // prefetch this warp's saved gelu'(Z) boxes while the MMAs still run
+      if (zbox_epi) {
+        // prefetch this warp's saved gelu'(Z) (or addend) boxes while the MMAs still run
         if (lane == 0) {
           bulk_wait_read<0>();  // the previous tile's stores have left the boxes
 #pragma unroll
@@ -643,21 +646,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               store_box(&em.d2, stg + 4096, col, c1, c2);
               bulk_commit();
             }
-          } else {  // GeluBwd: dZ = dH * gelu'(Z), written over the loaded box
+          } else {  // GeluBwd: dZ = dH * gelu'(Z); AddBF16: D = acc + Zin; over the loaded box
             uint8_t* box = stg + pc * 4096;
             mbar_wait(&zb[pc], zph[pc]);
             zph[pc] ^= 1u;
             uint4* br = box_row(box);
+            const bool add = p.epi == static_cast<int>(Epi::AddBF16);
+            auto op = [&](float a, float z) { return add ? a + z : a * z; };
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               uint4 gw = br[k ^ sw];
               const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gw);
               float2 g0 = __bfloat1622float2(g2[0]), g1 = __bfloat1622float2(g2[1]);
               float2 g2f = __bfloat1622float2(g2[2]), g3 = __bfloat1622float2(g2[3]);
-              br[k ^ sw] = make_uint4(pk(val(8 * k) * g0.x, val(8 * k + 1) * g0.y),
-                                      pk(val(8 * k + 2) * g1.x, val(8 * k + 3) * g1.y),
-                                      pk(val(8 * k + 4) * g2f.x, val(8 * k + 5) * g2f.y),
-                                      pk(val(8 * k + 6) * g3.x, val(8 * k + 7) * g3.y));
+              br[k ^ sw] = make_uint4(pk(op(val(8 * k), g0.x), op(val(8 * k + 1), g0.y)),
+                                      pk(op(val(8 * k + 2), g1.x), op(val(8 * k + 3), g1.y)),
+                                      pk(op(val(8 * k + 4), g2f.x), op(val(8 * k + 5), g2f.y)),
+                                      pk(op(val(8 * k + 6), g3.x), op(val(8 * k + 7), g3.y)));
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -947,7 +952,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     const int want = pr.force_bn;
     if (want == 128 && pr.epi != Epi::SwigluFwd && pr.epi != Epi::SwigluBwd) BN = 128;
     else if (want == 256) BN = 256;
-    else if (want == 512 && ctas == 2 && pr.epi != Epi::GeluBwd) BN = 512;
+    else if (want == 512 && ctas == 2 && pr.epi != Epi::GeluBwd && pr.epi != Epi::AddBF16) BN = 512;
   }
   const int bm = 128 * ctas, bn_seg = (BN < 256 ? BN : 256) / ctas;  // B box rows per segment
   if (pr.kind == GemmKind::RowGrouped) {
@@ -1015,7 +1020,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
         return cudaErrorInvalidValue;
     }
     const bool tma_epi = pr.epi == Epi::StoreBF16 || pr.epi == Epi::StoreF32 ||
-                         pr.epi == Epi::GeluFwd || pr.epi == Epi::GeluBwd;
+                         pr.epi == Epi::GeluFwd || pr.epi == Epi::GeluBwd || pr.epi == Epi::AddBF16;
     if (tma_epi) {
       if (pr.kind == GemmKind::RowGrouped) {
         const uint64_t rows_end = static_cast<uint64_t>(p.row0) + pr.rows;
@@ -1032,7 +1037,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
             !make_map3s(&em.d2, pr.D2, false, pr.N, rows_end, pr.nblk, pr.ldd2 * 2,
                         static_cast<uint64_t>(p.rows_total) * pr.ldd2 * 2, 64, 32))
           return cudaErrorInvalidValue;
-        if (pr.epi == Epi::GeluBwd &&
+        if ((pr.epi == Epi::GeluBwd || pr.epi == Epi::AddBF16) &&
             !make_map3s(&em.z, pr.Zin, false, pr.N, rows_end, pr.nblk, pr.ldz * 2,
                         static_cast<uint64_t>(p.rows_total) * pr.ldz * 2, 64, 32))
           return cudaErrorInvalidValue;

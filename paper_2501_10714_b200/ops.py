@@ -14,7 +14,7 @@ from . import _native as NL
 GATE_KINDS = {"noisy_topk": 0, "sigmoid_topk": 1, "cosine_topk": 2, "expert_choice": 3}
 DTYPES = {torch.float64: 0, torch.float32: 1, torch.bfloat16: 2}
 EPI = {"store_bf16": 0, "store_f32": 1, "gelu_fwd": 2, "swiglu_fwd": 3, "gelu_bwd": 4,
-       "swiglu_bwd": 5}
+       "swiglu_bwd": 5, "add_bf16": 6}
 
 
 def _ptr(t):

@@ -156,6 +156,38 @@ def test_gelu_epilogues():
     assert _rel(dZ, g) < 2e-2
 
 
+@pytest.mark.parametrize("inplace", [True, False])
+def test_add_bf16_epilogue(inplace):
+    """D = bf16(acc + Zin): exact on integer-valued operands (every product,
+    sum and the final add are exact), in place (Zin = D, the gate backward's
+    dx accumulation) and out of place, ragged rows."""
+    ops = _ops()
+    torch.manual_seed(1)
+    nblk, rows, K, N = 2, 300, 64, 320
+    A = torch.randint(-4, 5, (nblk, rows, K), device="cuda").to(torch.bfloat16)
+    B = torch.randint(-4, 5, (nblk, N, K), device="cuda").to(torch.bfloat16)
+    Z0 = torch.randint(-64, 65, (nblk, rows, N), device="cuda").to(torch.bfloat16)
+    Z = Z0.clone()
+    D = Z if inplace else torch.empty_like(Z)
+    ops.grouped_gemm("row", A, B, D, nblk=nblk, rows=rows, K=K, N=N, n_w=nblk, epi="add_bf16",
+                     Zin=Z, ldz=N)
+    torch.cuda.synchronize()
+    ref = (torch.stack([A[b].float() @ B[b].float().T for b in range(nblk)]) + Z0.float()).bfloat16()
+    assert torch.equal(D, ref)
+    if not inplace:
+        assert torch.equal(Z, Z0)
+    # random operands: within bf16 rounding of the fp32 result
+    A = _rand(nblk, rows, K)
+    B = _rand(nblk, N, K, scale=K ** -0.5)
+    Z0 = _rand(nblk, rows, N)
+    D = Z0.clone()
+    ops.grouped_gemm("row", A, B, D, nblk=nblk, rows=rows, K=K, N=N, n_w=nblk, epi="add_bf16",
+                     Zin=D, ldz=N)
+    torch.cuda.synchronize()
+    ref = torch.stack([A[b].float() @ B[b].float().T for b in range(nblk)]) + Z0.float()
+    assert _rel(D, ref) < 1e-2
+
+
 @pytest.mark.parametrize("H", [256, 640])
 def test_swiglu_epilogues(H):
     ops = _ops()
