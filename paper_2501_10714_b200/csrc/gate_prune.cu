@@ -843,8 +843,8 @@ __global__ void __launch_bounds__(512 + SC_MT_WARPS * 32)
 // (1 + 2^-8) |x| . |W|), and the reference's own fp64 sequential rounding —
 // all times |x|_2 |W_e|_2 (Cauchy-Schwarz), as before.
 constexpr int TC_COLS = 128;  // GEMM output columns (2 NC <= 128)
-constexpr int ST_TOK = 32;    // tokens per screen_tc block (4 threads each + one noise-draw warp)
-constexpr int ST_MAIN = 4 * ST_TOK;
+constexpr int ST_TOK = 32;    // tokens per screen_tc block (8 threads each + one noise-draw warp)
+constexpr int ST_MAIN = 8 * ST_TOK;
 constexpr int ST_TPT = ST_MAIN / ST_TOK;
 
 template <int KIND, int E_MAX>
