@@ -28,6 +28,7 @@ using namespace fsmoe_dev;
 __global__ void dscore_token_kernel(int kind, int T, int E, int k, const int* __restrict__ pexp,
                                     const double* __restrict__ pw, const double* __restrict__ dw,
                                     double* __restrict__ dS) {
+  fsmoe_dev::pdl_enter();
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   double* row = dS + static_cast<long long>(t) * E;
@@ -69,6 +70,7 @@ __global__ void dscore_ec_kernel(int T, int E, int C, const int* __restrict__ pt
 __global__ void noisy_dz_kernel(long long n, const double* __restrict__ dS,
                                 const double* __restrict__ noise, const double* __restrict__ spread,
                                 double* __restrict__ dZ) {
+  fsmoe_dev::pdl_enter();
   long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i < n) dZ[i] = dS[i] * noise[i] / (1.0 + exp(-spread[i]));
 }
@@ -648,6 +650,7 @@ __device__ __forceinline__ double gval(int c, int NC, long long t, const double*
 __global__ void g_split_kernel(int T, int NC, int NC2, int No, int Kp, const double* __restrict__ G1,
                                const double* __restrict__ G2, long long gst, long long gsc,
                                __nv_bfloat16* __restrict__ Gx, __nv_bfloat16* __restrict__ Gd) {
+  fsmoe_dev::pdl_enter();
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const int W = No > Kp ? No : Kp;
   if (i >= static_cast<long long>(T) * W) return;
@@ -669,6 +672,7 @@ __global__ void g_split_kernel(int T, int NC, int NC2, int No, int Kp, const dou
 __global__ void w_split_kernel(int M, int NC, int NC2, int Kp, const double* __restrict__ W1,
                                const double* __restrict__ W2, long long wsj, long long wsc,
                                __nv_bfloat16* __restrict__ Wd) {
+  fsmoe_dev::pdl_enter();
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<long long>(M) * Kp) return;
   const long long j = i / Kp;
@@ -685,6 +689,7 @@ __global__ void w_split_kernel(int M, int NC, int NC2, int Kp, const double* __r
 __global__ void xtg_tc_reduce_kernel(int S, int M, int NC, int NC2, int No, const float* __restrict__ P,
                                      double* __restrict__ out1, double* __restrict__ out2, long long osj,
                                      long long osc, int accumulate) {
+  fsmoe_dev::pdl_enter();
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<long long>(M) * NC2) return;
   const int j = static_cast<int>(i / NC2), c = static_cast<int>(i % NC2);
@@ -744,11 +749,11 @@ int gate_bwd_tc(int xdt, int T, int M, int NC, const void* X, const double* G1, 
   auto* Wd = reinterpret_cast<__nv_bfloat16*>(take(static_cast<size_t>(M) * sh.Kp * 2));
   auto* P = reinterpret_cast<float*>(take(static_cast<size_t>(sh.S) * M * sh.No * 4));
   const long long ng = static_cast<long long>(T) * (sh.No > sh.Kp ? sh.No : sh.Kp);
-  g_split_kernel<<<static_cast<int>((ng + 255) / 256), 256, 0, st>>>(T, NC, NC2, sh.No, sh.Kp, G1, G2 ? G2 : G1,
+  pdl_launch(g_split_kernel, static_cast<int>((ng + 255) / 256), 256, 0, st, T, NC, NC2, sh.No, sh.Kp, G1, G2 ? G2 : G1,
                                                                      gst, gsc, Gx, Gd);
   ::fsmoe::count_launch();
   const long long nw = static_cast<long long>(M) * sh.Kp;
-  w_split_kernel<<<static_cast<int>((nw + 255) / 256), 256, 0, st>>>(M, NC, NC2, sh.Kp, W1, W2 ? W2 : W1, wsj,
+  pdl_launch(w_split_kernel, static_cast<int>((nw + 255) / 256), 256, 0, st, M, NC, NC2, sh.Kp, W1, W2 ? W2 : W1, wsj,
                                                                      wsc, Wd);
   ::fsmoe::count_launch();
   // x^T G: S blocks of T/S tokens, each its own output block (n_w = S)
@@ -769,7 +774,7 @@ int gate_bwd_tc(int xdt, int T, int M, int NC, const void* X, const double* G1, 
   int rc = gemm_sm100_launch(g, st);
   if (rc != cudaSuccess) return cuda_status(static_cast<cudaError_t>(rc), "gate backward x^T G (tcgen05)");
   const long long nr = static_cast<long long>(M) * NC2;
-  xtg_tc_reduce_kernel<<<static_cast<int>((nr + 255) / 256), 256, 0, st>>>(sh.S, M, NC, NC2, sh.No, P, out1,
+  pdl_launch(xtg_tc_reduce_kernel, static_cast<int>((nr + 255) / 256), 256, 0, st, sh.S, M, NC, NC2, sh.No, P, out1,
                                                                            out2 ? out2 : out1, osj, osc, 1);
   ::fsmoe::count_launch();
   // dx += Gd . Wd^T, in place through the AddBF16 epilogue
@@ -844,10 +849,10 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
   double* tw = tcw ? w.take(tcw) : nullptr;
   switch (d.kind) {
     case FSMOE_GATE_NOISY_TOPK: {
-      dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
+      pdl_launch(dscore_token_kernel, (T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st, 0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dZ = w.take(static_cast<size_t>(T) * E);
       long long n = static_cast<long long>(T) * E;
-      noisy_dz_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(n, dS, noise, spread, dZ); ::fsmoe::count_launch();
+      pdl_launch(noisy_dz_kernel, static_cast<int>((n + 255) / 256), 256, 0, st, n, dS, noise, spread, dZ); ::fsmoe::count_launch();
       const int tc = gate_bwd_tc(d.x_dtype, T, M, E, x, dS, dZ, E, 1, dWs, dWn, E, 1, w_score, w_noise, E, 1,
                                  dx, tw, st);
       if (tc >= 0) {
@@ -865,7 +870,7 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       break;
     }
     case FSMOE_GATE_SIGMOID_TOPK: {
-      dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(1, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
+      pdl_launch(dscore_token_kernel, (T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st, 1, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       const int tc = gate_bwd_tc(d.x_dtype, T, M, E, x, dS, nullptr, E, 1, dWs, nullptr, E, 1, w_score, nullptr,
                                  E, 1, dx, tw, st);
       if (tc >= 0) {
@@ -884,7 +889,7 @@ int gate_bwd_launch(const fsmoe_gate_desc& d, const void* x, const double* w_sco
       break;
     }
     case FSMOE_GATE_COSINE_TOPK: {
-      dscore_token_kernel<<<(T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st>>>(0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
+      pdl_launch(dscore_token_kernel, (T + per_token_block(T) - 1) / per_token_block(T), per_token_block(T), 0, st, 0, T, E, k, pexp, pw, dw, dS); ::fsmoe::count_launch();
       double* dq = w.take(static_cast<size_t>(T) * P);
       double* qn = w.take(static_cast<size_t>(T) * P);
       double* en = w.take(E);

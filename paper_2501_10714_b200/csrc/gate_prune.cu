@@ -64,6 +64,7 @@ __global__ void w_prep_kernel(int M, int Ea, const double* __restrict__ Wa, int 
                               const double* __restrict__ Wb, float* __restrict__ W32,
                               double* __restrict__ WT, double* __restrict__ wn,
                               __nv_bfloat16* __restrict__ Wtc) {
+  fsmoe_dev::pdl_enter();
   const int NC = Ea + Eb;
   const int c = blockIdx.x;
   double ss = 0.0;
@@ -854,6 +855,7 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
                      double gam, uint64_t seed, double* __restrict__ noise_ws,
                      double* __restrict__ scores_out, double* __restrict__ spread_out,
                      uint64_t* __restrict__ mask) {
+  fsmoe_dev::pdl_enter();
   __shared__ uint64_t draws[KIND == 0 ? ST_TOK * 2 * E_MAX : 1];
   __shared__ float nrm[ST_MAIN];  // [token][ST_TPT partial sums]
   __shared__ double lo[ST_TOK * E_MAX], hi[ST_TOK * E_MAX];
@@ -1002,6 +1004,7 @@ __global__ void __launch_bounds__(XF_THREADS)
                        const double* __restrict__ noise, int* __restrict__ pick_token,
                        int* __restrict__ pick_expert, double* __restrict__ pick_weight,
                        double* __restrict__ scores_out, double* __restrict__ spread_out) {
+  fsmoe_dev::pdl_enter();
   constexpr int NPROJ = KIND == 0 ? 2 : 1;
   using S = XfSmem<NPROJ, E_MAX>;
   extern __shared__ __align__(16) uint8_t sm[];
@@ -1352,7 +1355,7 @@ void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const floa
   // E's stages (at least the certain-pick path's dot / bound scratch)
   const int xs_rt = std::max(XfSmem<KIND == 0 ? 2 : 1, E_MAX>::NS * XfSmem<KIND == 0 ? 2 : 1, E_MAX>::stride(E),
                              XF_TOK * E_MAX * 2 * 8 * 2);
-  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st>>>(
+  pdl_launch(exact_final_kernel<KIND, E_MAX>, (T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st, 
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
       spread_out);
   ::fsmoe::count_launch();
@@ -1385,7 +1388,7 @@ void launch_fused_tc(const fsmoe_gate_desc& d, const void* x, const __nv_bfloat1
   const double cB = gamp * (1.0 + 0x1.0p-8) * 1.01 + 0x1.0p-18 + (M + 2.0) * 0x1.0p-53;
   const double gam = M * 0x1.0p-24 / (1.0 - M * 0x1.0p-24);  // fp32 |x|^2 sums
   const auto* xb = static_cast<const __nv_bfloat16*>(x);
-  screen_tc_kernel<KIND, E_MAX><<<(T + ST_TOK - 1) / ST_TOK, ST_MAIN + 32, 0, st>>>(
+  pdl_launch(screen_tc_kernel<KIND, E_MAX>, (T + ST_TOK - 1) / ST_TOK, ST_MAIN + 32, 0, st, 
       xb, T, M, E, k, P, wn, cB, gam, d.seed, noise_ws, scores_out, spread_out, mask);
   ::fsmoe::count_launch();
   constexpr int XSMEM = XfSmem<KIND == 0 ? 2 : 1, E_MAX>::BYTES;
@@ -1394,7 +1397,7 @@ void launch_fused_tc(const fsmoe_gate_desc& d, const void* x, const __nv_bfloat1
   // E's stages (at least the certain-pick path's dot / bound scratch)
   const int xs_rt = std::max(XfSmem<KIND == 0 ? 2 : 1, E_MAX>::NS * XfSmem<KIND == 0 ? 2 : 1, E_MAX>::stride(E),
                              XF_TOK * E_MAX * 2 * 8 * 2);
-  exact_final_kernel<KIND, E_MAX><<<(T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st>>>(
+  pdl_launch(exact_final_kernel<KIND, E_MAX>, (T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st, 
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
       spread_out);
   ::fsmoe::count_launch();
@@ -1479,7 +1482,7 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
   // bf16 hi / lo split of W); FSMOE_GATE_SIMT keeps the fp32 FFMA2 screen
   const bool tc = fused && 2 * NC <= TC_COLS && !getenv("FSMOE_GATE_SIMT");
   if (tc) FSMOE_CUDA_TRY(cudaMemsetAsync(w.Wtc, 0, 2ull * TC_COLS * M, st), "gate memset");
-  w_prep_kernel<<<NC, 256, 0, st>>>(M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn,
+  pdl_launch(w_prep_kernel, NC, 256, 0, st, M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn,
                                     tc ? w.Wtc : nullptr);
   ::fsmoe::count_launch();
   if (tc) {

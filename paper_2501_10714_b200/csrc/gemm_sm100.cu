@@ -330,6 +330,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: the prologue above (barriers, TMEM,
+  // descriptor prefetch) overlapped the previous kernel's tail; nothing
+  // below may touch global memory before it has completed
+  fsmoe_dev::pdl_enter();
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA loads its half) ==========
@@ -1060,13 +1064,22 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ctas;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (ctas == 2) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = ctas;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    if (pdl_on()) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = ctas == 2 ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, ta, tb, p, em);
   };
   cudaError_t e;

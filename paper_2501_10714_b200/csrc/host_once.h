@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
+#include <utility>
 
 namespace fsmoe {
 
@@ -48,6 +50,35 @@ inline int device_sms() {
 // the latency-bound per-token loops over every SM).
 inline int per_token_block(long long T) {
   return (T + 127) / 128 >= 2LL * device_sms() ? 128 : 32;
+}
+
+// Programmatic dependent launch (PDL). Kernels that start with
+// fsmoe_dev::pdl_enter() are launched through pdl_launch() with
+// cudaLaunchAttributeProgrammaticStreamSerialization: the next kernel of the
+// stream is scheduled while this one drains (its prologue overlaps our tail)
+// and blocks in griddepcontrol.wait until this grid has completed and its
+// memory is visible. FSMOE_PDL=0 turns the attribute off (read once).
+inline bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("FSMOE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... P, typename... A>
+cudaError_t pdl_launch(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
 }  // namespace fsmoe

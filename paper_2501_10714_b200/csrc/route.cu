@@ -42,6 +42,7 @@ constexpr int AS_CNT_CACHE = 2048;  // tile histograms kept in shared memory (in
 __global__ void __launch_bounds__(AS_THREADS)
     assign_count_kernel(long long P, const int* __restrict__ ptok, const int* __restrict__ pexp,
                         int T, int E, int* __restrict__ cnt, int* __restrict__ status) {
+  fsmoe_dev::pdl_enter();
   __shared__ int h[AS_MAX_E];
   for (int i = threadIdx.x; i < E; i += AS_THREADS) h[i] = 0;
   __syncthreads();
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(AS_THREADS)
                        const int* __restrict__ cnt, int ntiles, int* __restrict__ slot_of_pick,
                        int* __restrict__ pick_of_slot, long long* __restrict__ fill,
                        long long* __restrict__ dropped) {
+  fsmoe_dev::pdl_enter();
   __shared__ int base[AS_MAX_E];
   __shared__ int wc[AS_THREADS / 32][AS_MAX_E];
   __shared__ int cs[AS_CNT_CACHE];
@@ -135,6 +137,7 @@ __global__ void __launch_bounds__(AS_THREADS)
 // ------------------------------------------------------ token index (CSR) --
 
 __global__ void tok_token_major_kernel(int T, int k, int* __restrict__ ptr, int* __restrict__ idx) {
+  fsmoe_dev::pdl_enter();
   long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i <= T) ptr[i] = static_cast<int>(i * k);
   if (i < static_cast<long long>(T) * k) idx[i] = static_cast<int>(i);
@@ -218,6 +221,7 @@ __global__ void __launch_bounds__(256)
     dispatch_kernel(long long n_slots, int row_vecs, int E, long long C, int chunks,
                     const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
                     const V* __restrict__ x, const PeerRows buf, const RowRange rr) {
+  fsmoe_dev::pdl_enter();
   const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (s >= n_slots || !in_range(rr, s)) return;
   const int lane = threadIdx.x & 31;
@@ -251,6 +255,7 @@ __global__ void __launch_bounds__(32)
     dispatch_bulk_kernel(long long n_slots, int row_bytes, int E, long long C, int chunks,
                          const int* __restrict__ pick_of_slot, const int* __restrict__ ptok,
                          const uint8_t* __restrict__ x, const PeerRows buf, const RowRange rr) {
+  fsmoe_dev::pdl_enter();
   extern __shared__ __align__(128) uint8_t sm[];  // [BK_ROWS][row_bytes] + one zero row
   // one mbarrier per lane: a row's store leaves as soon as that row has landed
   // instead of after the whole group of BK_ROWS rows
@@ -296,6 +301,7 @@ __global__ void __launch_bounds__(32)
 __global__ void __launch_bounds__(32)
     gather_bulk_kernel(long long n_rows, int row_bytes, const int* __restrict__ idx,
                        const uint8_t* __restrict__ src, const PeerRows dst) {
+  fsmoe_dev::pdl_enter();
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ __align__(8) uint64_t bar[BK_ROWS];  // one per lane, as in dispatch_bulk_kernel
   const int lane = threadIdx.x;
@@ -506,6 +512,7 @@ __global__ void __launch_bounds__(256)
     combine_kernel(int ntok, int M, int E, long long C, int chunks, const int* __restrict__ tptr,
                    const int* __restrict__ tpick, const int* __restrict__ slot_of_pick,
                    const double* __restrict__ pw, const T* __restrict__ buf, T* __restrict__ y) {
+  fsmoe_dev::pdl_enter();
   using A = typename Acc<T>::type;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= ntok) return;
@@ -550,6 +557,7 @@ __global__ void __launch_bounds__(256)
                         const int* __restrict__ tptr, const int* __restrict__ tpick,
                         const int* __restrict__ slot_of_pick, const T* __restrict__ dbuf,
                         T* __restrict__ dx, int accumulate) {
+  fsmoe_dev::pdl_enter();
   using A = typename Acc<T>::type;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= ntok) return;
@@ -599,6 +607,7 @@ __global__ void __launch_bounds__(256)
                        const double* __restrict__ pw, const T* __restrict__ dy,
                        const T* __restrict__ buf, const PeerRows dbuf, double* __restrict__ dw,
                        const RowRange rr) {
+  fsmoe_dev::pdl_enter();
   using A = typename Acc<T>::type;
   const long long s = blockIdx.x * 8LL + (threadIdx.x >> 5);
   if (s >= n_slots || !in_range(rr, s)) return;
@@ -679,8 +688,8 @@ int assign_launch(long long P, const int* ptok, const int* pexp, int T, int E, l
   }
   int ntiles = static_cast<int>((P + AS_TILE - 1) / AS_TILE);
   int* cnt = static_cast<int*>(ws);
-  assign_count_kernel<<<ntiles, AS_THREADS, 0, st>>>(P, ptok, pexp, T, E, cnt, status); ::fsmoe::count_launch();
-  assign_rank_kernel<<<ntiles, AS_THREADS, 0, st>>>(P, pexp, E, C, cnt, ntiles, slot_of_pick,
+  pdl_launch(assign_count_kernel, ntiles, AS_THREADS, 0, st, P, ptok, pexp, T, E, cnt, status); ::fsmoe::count_launch();
+  pdl_launch(assign_rank_kernel, ntiles, AS_THREADS, 0, st, P, pexp, E, C, cnt, ntiles, slot_of_pick,
                                                     pick_of_slot, fill, dropped); ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_assign");
 }
@@ -693,7 +702,7 @@ int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, in
                        void* ws, cudaStream_t st) {
   if (k > 0) {
     long long n = (static_cast<long long>(T) * k > T + 1) ? static_cast<long long>(T) * k : T + 1;
-    tok_token_major_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(T, k, tptr, tpick); ::fsmoe::count_launch();
+    pdl_launch(tok_token_major_kernel, static_cast<int>((n + 255) / 256), 256, 0, st, T, k, tptr, tpick); ::fsmoe::count_launch();
     return cuda_status(cudaGetLastError(), "fsmoe_token_index");
   }
   int* cnt = static_cast<int*>(ws);
@@ -715,7 +724,7 @@ int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, co
   static DeviceOnce attr;
   once_on_device(attr, [&] { cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096); });
   const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
-  gather_bulk_kernel<<<bulk_grid(gather_bulk_kernel, smem, (n_rows + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
+  pdl_launch(gather_bulk_kernel, bulk_grid(gather_bulk_kernel, smem, (n_rows + BK_ROWS - 1) / BK_ROWS), 32, smem, st, 
       n_rows, static_cast<int>(row_bytes), idx, static_cast<const uint8_t*>(src), dst);
   ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_gather_rows");
@@ -728,24 +737,25 @@ int dispatch_launch(int dtype, int M, int E, long long C, int chunks, const int*
   if (n_slots <= 0 || M <= 0) return FSMOE_OK;
   const long long row_bytes = static_cast<long long>(M) * elem_size(dtype);
   const int grid = static_cast<int>((n_slots + 7) / 8);
-  if (row_bytes % 16 == 0 && row_bytes <= 4096 && !getenv("FSMOE_ROUTE_NOBULK")) {
+  static const bool nobulk = getenv("FSMOE_ROUTE_NOBULK") != nullptr;  // measurement switch, read once
+  if (row_bytes % 16 == 0 && row_bytes <= 4096 && !nobulk) {
     const int smem = static_cast<int>((BK_ROWS + 1) * row_bytes);
     static DeviceOnce attr;
     once_on_device(attr, [&] { cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 4096); });
-    dispatch_bulk_kernel<<<bulk_grid(dispatch_bulk_kernel, smem, (n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st>>>(
+    pdl_launch(dispatch_bulk_kernel, bulk_grid(dispatch_bulk_kernel, smem, (n_slots + BK_ROWS - 1) / BK_ROWS), 32, smem, st, 
         n_slots, static_cast<int>(row_bytes), E, C, chunks, pick_of_slot, ptok,
         static_cast<const uint8_t*>(x), buf, rr);
     ::fsmoe::count_launch();
   } else if (row_bytes % 16 == 0) {
-    dispatch_kernel<uint4><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 16), E, C,
+    pdl_launch(dispatch_kernel<uint4>, grid, 256, 0, st, n_slots, static_cast<int>(row_bytes / 16), E, C,
                                                  chunks, pick_of_slot, ptok,
                                                  static_cast<const uint4*>(x), buf, rr); ::fsmoe::count_launch();
   } else if (row_bytes % 8 == 0) {
-    dispatch_kernel<uint2><<<grid, 256, 0, st>>>(n_slots, static_cast<int>(row_bytes / 8), E, C,
+    pdl_launch(dispatch_kernel<uint2>, grid, 256, 0, st, n_slots, static_cast<int>(row_bytes / 8), E, C,
                                                  chunks, pick_of_slot, ptok,
                                                  static_cast<const uint2*>(x), buf, rr); ::fsmoe::count_launch();
   } else {
-    dispatch_kernel<uint16_t><<<grid, 256, 0, st>>>(
+    pdl_launch(dispatch_kernel<uint16_t>, grid, 256, 0, st, 
         n_slots, static_cast<int>(row_bytes / 2), E, C, chunks, pick_of_slot, ptok,
         static_cast<const uint16_t*>(x), buf, rr); ::fsmoe::count_launch();
   }
@@ -760,10 +770,10 @@ int combine_launch(int dtype, int T, int M, int E, long long C, int chunks, cons
   int rc = by_dtype(dtype, [&](auto tag) {
     using Tt = decltype(tag);
     if (M % CV == 0)
-      combine_kernel<Tt, true><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+      pdl_launch(combine_kernel<Tt, true>, grid, 256, 0, st, T, M, E, C, chunks, tptr, tpick, slot_of_pick,
                                                      pw, static_cast<const Tt*>(buf), static_cast<Tt*>(y));
     else
-      combine_kernel<Tt, false><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+      pdl_launch(combine_kernel<Tt, false>, grid, 256, 0, st, T, M, E, C, chunks, tptr, tpick, slot_of_pick,
                                                       pw, static_cast<const Tt*>(buf), static_cast<Tt*>(y));
     ::fsmoe::count_launch();
   });
@@ -779,11 +789,11 @@ int dispatch_bwd_launch(int dtype, int T, int M, int E, long long C, int chunks,
   int rc = by_dtype(dtype, [&](auto tag) {
     using Tt = decltype(tag);
     if (M % CV == 0)
-      dispatch_bwd_kernel<Tt, true><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+      pdl_launch(dispatch_bwd_kernel<Tt, true>, grid, 256, 0, st, T, M, E, C, chunks, tptr, tpick, slot_of_pick,
                                                           static_cast<const Tt*>(dbuf),
                                                           static_cast<Tt*>(dx), accumulate);
     else
-      dispatch_bwd_kernel<Tt, false><<<grid, 256, 0, st>>>(T, M, E, C, chunks, tptr, tpick, slot_of_pick,
+      pdl_launch(dispatch_bwd_kernel<Tt, false>, grid, 256, 0, st, T, M, E, C, chunks, tptr, tpick, slot_of_pick,
                                                            static_cast<const Tt*>(dbuf),
                                                            static_cast<Tt*>(dx), accumulate);
     ::fsmoe::count_launch();
@@ -805,12 +815,12 @@ int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long lo
   int rc = by_dtype(dtype, [&](auto tag) {
     using Tt = decltype(tag);
     if (M % CV == 0)
-      combine_bwd_kernel<Tt, true><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
+      pdl_launch(combine_bwd_kernel<Tt, true>, grid, 256, 0, st, n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
                                                          static_cast<const Tt*>(dy),
                                                          static_cast<const Tt*>(buf),
                                                          dbuf, dw, rr);
     else
-      combine_bwd_kernel<Tt, false><<<grid, 256, 0, st>>>(n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
+      pdl_launch(combine_bwd_kernel<Tt, false>, grid, 256, 0, st, n_slots, M, E, C, chunks, pick_of_slot, ptok, pw,
                                                           static_cast<const Tt*>(dy),
                                                           static_cast<const Tt*>(buf),
                                                           dbuf, dw, rr);

@@ -23,6 +23,15 @@ __device__ __forceinline__ double load_as_double<2>(const void* base, long long 
   return static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]));
 }
 
+// Programmatic dependent launch (host side: fsmoe::pdl_launch): let the
+// stream's next kernel be scheduled now, then wait until every prior grid has
+// completed and its memory is visible. Must precede any global-memory access
+// of a kernel launched with the PDL attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Reference arithmetic: acc + a*b with a separately rounded product (no FMA).
 __device__ __forceinline__ double mul_add_rn(double acc, double a, double b) {
   return __dadd_rn(acc, __dmul_rn(a, b));
