@@ -67,6 +67,11 @@ __global__ void w_prep_kernel(int M, int Ea, const double* __restrict__ Wa, int 
   fsmoe_dev::pdl_enter();
   const int NC = Ea + Eb;
   const int c = blockIdx.x;
+  if (c >= NC) {  // blocks past the columns zero Wtc's unused rows [2 NC, ...)
+    __nv_bfloat16* r = Wtc + static_cast<long long>(NC + c) * M;
+    for (int j = threadIdx.x; j < M; j += blockDim.x) r[j] = __float2bfloat16(0.f);
+    return;
+  }
   double ss = 0.0;
   // eight rows' loads in flight per thread before their uses (the column is
   // strided in W: each load is its own line, so latency dominates)
@@ -1481,8 +1486,8 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
   // the approximate scores on the tensor cores (tcgen05 GEMM of x against the
   // bf16 hi / lo split of W); FSMOE_GATE_SIMT keeps the fp32 FFMA2 screen
   const bool tc = fused && 2 * NC <= TC_COLS && !getenv("FSMOE_GATE_SIMT");
-  if (tc) FSMOE_CUDA_TRY(cudaMemsetAsync(w.Wtc, 0, 2ull * TC_COLS * M, st), "gate memset");
-  pdl_launch(w_prep_kernel, NC, 256, 0, st, M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn,
+  // (with the tensor-core screen, blocks NC.. zero Wtc's padding rows 2 NC..TC_COLS)
+  pdl_launch(w_prep_kernel, tc ? TC_COLS - NC : NC, 256, 0, st, M, E, w_score, noisy ? E : 0, w_noise, w.W32, w.WT, w.wn,
                                     tc ? w.Wtc : nullptr);
   ::fsmoe::count_launch();
   if (tc) {

@@ -41,8 +41,13 @@ constexpr int AS_CNT_CACHE = 2048;  // tile histograms kept in shared memory (in
 // cnt[tile][e] = picks of expert e inside the tile; flags bad picks.
 __global__ void __launch_bounds__(AS_THREADS)
     assign_count_kernel(long long P, const int* __restrict__ ptok, const int* __restrict__ pexp,
-                        int T, int E, int* __restrict__ cnt, int* __restrict__ status) {
+                        int T, int E, int* __restrict__ cnt, int* __restrict__ status,
+                        int* __restrict__ pick_of_slot, long long n_slots) {
   fsmoe_dev::pdl_enter();
+  // every slot starts empty (assign_rank, the next kernel, fills the kept ones)
+  for (long long i = blockIdx.x * static_cast<long long>(AS_THREADS) + threadIdx.x; i < n_slots;
+       i += static_cast<long long>(gridDim.x) * AS_THREADS)
+    pick_of_slot[i] = -1;
   __shared__ int h[AS_MAX_E];
   for (int i = threadIdx.x; i < E; i += AS_THREADS) h[i] = 0;
   __syncthreads();
@@ -680,15 +685,16 @@ int assign_launch(long long P, const int* ptok, const int* pexp, int T, int E, l
                   int* slot_of_pick, long long* fill, long long* dropped, int* pick_of_slot,
                   int* status, void* ws, cudaStream_t st) {
   if (E > AS_MAX_E) return config_error("dispatch: at most 256 experts per rank supported");
-  FSMOE_CUDA_TRY(cudaMemsetAsync(pick_of_slot, 0xFF, sizeof(int) * E * C, st), "assign memset");
   if (P <= 0) {
+    FSMOE_CUDA_TRY(cudaMemsetAsync(pick_of_slot, 0xFF, sizeof(int) * E * C, st), "assign memset");
     FSMOE_CUDA_TRY(cudaMemsetAsync(fill, 0, sizeof(long long) * E, st), "assign memset");
     FSMOE_CUDA_TRY(cudaMemsetAsync(dropped, 0, sizeof(long long), st), "assign memset");
     return FSMOE_OK;
   }
   int ntiles = static_cast<int>((P + AS_TILE - 1) / AS_TILE);
   int* cnt = static_cast<int*>(ws);
-  pdl_launch(assign_count_kernel, ntiles, AS_THREADS, 0, st, P, ptok, pexp, T, E, cnt, status); ::fsmoe::count_launch();
+  pdl_launch(assign_count_kernel, ntiles, AS_THREADS, 0, st, P, ptok, pexp, T, E, cnt, status, pick_of_slot,
+             static_cast<long long>(E) * C); ::fsmoe::count_launch();
   pdl_launch(assign_rank_kernel, ntiles, AS_THREADS, 0, st, P, pexp, E, C, cnt, ntiles, slot_of_pick,
                                                     pick_of_slot, fill, dropped); ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_assign");
