@@ -26,12 +26,14 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(world, precision, gate, ffn, rf, rb, k=2, dense=0, split=None, T=1024, M=256, H=256,
-         transport=None):
+         transport=None, experts_per_rank=None):
     import layer_oracle
     import pyoracle
     from paper_2501_10714_b200.layer import EpGroup, MoEConfig, MoELayer, expert_params, gate_params, run_ranks
 
     E = 4 * world if gate != "expert_choice" else 2 * world
+    if experts_per_rank:
+        E = experts_per_rank * world
     slices = [dense // 3, dense // 3, dense - 2 * (dense // 3)] if dense else []
     cfg = MoEConfig(tokens=T, model_dim=M, ffn_dim=H, experts=E, top_k=k, gate=gate, ffn=ffn,
                     precision=precision, seed=9, r_fwd=rf, r_bwd=rb,
@@ -186,3 +188,11 @@ def test_local_ep_copy_engine_chunked_pipeline(world, precision, gate, ffn, rf, 
     chunk on the copy engines (fsmoe_peer_copy_rows) with stream-memory-op
     flags (fsmoe_peer_flag_write), GEMM chunk i waiting only for chunk i."""
     _run(world, precision, gate, ffn, rf, rb, k=k, transport="ce")
+
+
+@pytest.mark.parametrize("world,transport,rf,rb", [
+    (8, "peer", 1, 1), (8, "peer", 2, 2), (8, "ce", 2, 2), (4, "ce", 3, 2)])
+def test_local_ep_one_expert_per_rank(world, transport, rf, rb):
+    """configs[2] on 8 GPUs holds one expert per rank (E_l = 1): top-2 noisy
+    SwiGLU with both exchange transports and chunked pipelines."""
+    _run(world, "bf16", "noisy_topk", "gated3", rf, rb, transport=transport, experts_per_rank=1)
