@@ -980,7 +980,7 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
 }
 
 constexpr int XF_TOK = 64;       // tokens per exact/final block
-constexpr int XF_THREADS = 256;
+constexpr int XF_THREADS = 512;
 constexpr int XF_JC = 64;        // columns per stage
 constexpr int XF_XROW = XF_JC * 2 + 16;  // bf16 row bytes (+16: conflict-free LDS.128)
 constexpr int XF_WROW = XF_JC + 2;       // fp64 per W^T smem row (+16 B, same reason)
