@@ -980,7 +980,7 @@ __global__ void __launch_bounds__(ST_MAIN + 32)
 }
 
 constexpr int XF_TOK = 64;       // tokens per exact/final block
-constexpr int XF_THREADS = 512;
+constexpr int XF_THREADS = 256;
 constexpr int XF_JC = 64;        // columns per stage
 constexpr int XF_XROW = XF_JC * 2 + 16;  // bf16 row bytes (+16: conflict-free LDS.128)
 constexpr int XF_WROW = XF_JC + 2;       // fp64 per W^T smem row (+16 B, same reason)
@@ -990,8 +990,11 @@ struct XfSmem {
   static constexpr int XS = XF_TOK * XF_XROW;             // token rows of one stage
   static constexpr int WS = NPROJ * E_MAX * XF_WROW * 8;   // W^T rows (fp64) of one stage
   static constexpr int STAGE = XS + WS;
-  static constexpr int NS = 3;                               // stages in flight
-  static constexpr int BYTES = NS * STAGE;                   // at E = E_MAX
+  static constexpr int NS = 2;                               // stages in flight
+  static constexpr int BYTES_STAGES = NS * STAGE;            // at E = E_MAX
+  // the top-1 certain-pick path's dot / bound scratch (KIND 0 only) reuses it
+  static constexpr int CERT = NPROJ == 2 ? XF_TOK * E_MAX * 2 * 8 * 2 : 0;
+  static constexpr int BYTES = BYTES_STAGES > CERT ? BYTES_STAGES : CERT;  // the attribute
   // the launched stage stride holds the W^T rows of the E actual experts
   static __host__ __device__ int stride(int E) { return XS + NPROJ * E * XF_WROW * 8; }
 };
@@ -1236,7 +1239,8 @@ __global__ void __launch_bounds__(XF_THREADS)
     for (int i = 0; i < S::NS - 1; ++i) issue(i);  // every issue commits a group (maybe empty)
   for (int ck = 0; ck < nck; ++ck) {
     cp_async_wait<S::NS - 2>();  // chunk ck has landed
-    __syncthreads();
+    __syncthreads();             // ... for every thread, and chunk ck - 1's buffer is free
+    issue(ck + S::NS - 1);       // into that buffer, in flight while chunk ck is consumed
     const uint8_t* st = sm + (ck % S::NS) * stg;
     const double* ws = reinterpret_cast<const double*>(st + S::XS);
     auto run = [&](double (&acc)[NPROJ], short2 te) {
@@ -1251,8 +1255,6 @@ __global__ void __launch_bounds__(XF_THREADS)
     };
     if (it0 < nwork) run(acc0, te0);
     if (it1 < nwork) run(acc1, te1);
-    __syncthreads();
-    issue(ck + S::NS - 1);
   }
 #pragma unroll
   for (int pj = 0; pj < NPROJ; ++pj) {
@@ -1359,7 +1361,7 @@ void launch_fused(const fsmoe_gate_desc& d, const void* x, double cB, const floa
   once_on_device(xattr, [&] { cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM); });
   // E's stages (at least the certain-pick path's dot / bound scratch)
   const int xs_rt = std::max(XfSmem<KIND == 0 ? 2 : 1, E_MAX>::NS * XfSmem<KIND == 0 ? 2 : 1, E_MAX>::stride(E),
-                             XF_TOK * E_MAX * 2 * 8 * 2);
+                             XfSmem<KIND == 0 ? 2 : 1, E_MAX>::CERT);
   pdl_launch(exact_final_kernel<KIND, E_MAX>, (T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st, 
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
       spread_out);
@@ -1401,7 +1403,7 @@ void launch_fused_tc(const fsmoe_gate_desc& d, const void* x, const __nv_bfloat1
   once_on_device(xattr, [&] { cudaFuncSetAttribute(exact_final_kernel<KIND, E_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM); });
   // E's stages (at least the certain-pick path's dot / bound scratch)
   const int xs_rt = std::max(XfSmem<KIND == 0 ? 2 : 1, E_MAX>::NS * XfSmem<KIND == 0 ? 2 : 1, E_MAX>::stride(E),
-                             XF_TOK * E_MAX * 2 * 8 * 2);
+                             XfSmem<KIND == 0 ? 2 : 1, E_MAX>::CERT);
   pdl_launch(exact_final_kernel<KIND, E_MAX>, (T + XF_TOK - 1) / XF_TOK, XF_THREADS, xs_rt, st, 
       xb, T, M, E, k, WT, mask, noise_ws, pick_token, pick_expert, pick_weight, scores_out,
       spread_out);
@@ -1493,7 +1495,10 @@ int gate_prune_launch(const fsmoe_gate_desc& d, const void* x, const double* w_s
   if (tc) {
     double* nz = noise_out ? noise_out : w.noise;
     if (noisy) {
-      if (E <= 16) launch_fused_tc<0, 16>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+      // E_MAX sizes the exact phase's shared memory: E <= 8 (configs[2]) fits
+      // four 256-thread blocks per SM, so a 32k-token grid runs in one wave
+      if (E <= 8) launch_fused_tc<0, 8>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
+      else if (E <= 16) launch_fused_tc<0, 16>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
       else launch_fused_tc<0, 32>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
     } else {
       launch_fused_tc<1, 32>(d, x, w.Wtc, w.P, w.WT, w.wn, nz, w.mask, pick_token, pick_expert, pick_weight, scores_out, spread_out, st);
