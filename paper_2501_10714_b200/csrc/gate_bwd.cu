@@ -3,9 +3,12 @@
 //   d_weight -> d scores:  softmax over the kept set (noisy / cosine / EC),
 //                          logistic (sigmoid); dropped picks have d_weight 0 but
 //                          still couple through the softmax normaliser.
-//   d scores -> params:    dW = x^T dS (fp64, deterministic split-T reduction),
-//                          dx += dS W^T; noisy adds the softplus(x W_noise)*n
-//                          branch; cosine goes through q = P x and the norms.
+//   d scores -> params:    dW = x^T dS (deterministic split-T reduction, fp64
+//                          across splits), dx += dS W^T; noisy adds the
+//                          softplus(x W_noise)*n branch; cosine goes through
+//                          q = P x and the norms. For bf16 tokens the noisy /
+//                          sigmoid contractions run on the tcgen05 GEMM (see
+//                          "tensor-core forms" below), else SIMT FMA kernels.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
