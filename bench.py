@@ -170,6 +170,36 @@ def cpu_threads_for(T, M, E, cap):
     return int(max(1, min(cores, (0.6 * avail) // per)))
 
 
+def cpu_layer_restatement(M, H, gated, top_k, threads, tokens=256):
+    """The whole layer step on the host cores, for scale: a torch-CPU fp32
+    restatement (NOT the reference, which has no FFN or backward) of the
+    expert FFN forward + backward that every token runs top_k times (the
+    dominant cost; gate and permutations are timed by cpu_baseline). A
+    bounded sample: `tokens` tokens through top_k experts of the workload's
+    shape, fwd + bwd with autograd, best of 2. Returns (tokens/s, seconds)."""
+    import torch
+    torch.set_num_threads(threads)
+    g = torch.Generator().manual_seed(5)
+    n1 = 2 * H if gated else H
+    x = torch.rand(tokens, M, generator=g) * 2 - 1
+    ws = [((torch.rand(n1, M, generator=g) * 2 - 1) / M ** 0.5).requires_grad_(True) for _ in range(top_k)]
+    w2 = [((torch.rand(M, H, generator=g) * 2 - 1) / H ** 0.5).requires_grad_(True) for _ in range(top_k)]
+    dy = torch.rand(tokens, M, generator=g) * 2 - 1
+    best = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        xi = x.clone().requires_grad_(True)
+        y = 0
+        for e in range(top_k):
+            z = xi @ ws[e].T
+            h = torch.nn.functional.silu(z[:, :H]) * z[:, H:] if gated else torch.nn.functional.gelu(z)
+            y = y + h @ w2[e].T
+        y.backward(dy)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return tokens / best, best
+
+
 def cpu_reference_pass(threads, x, w_gate, w_noise, experts, top_k, capacity):
     """The reference's own implementation of the path (run_gate -> dispatch_tokens
     -> combine_tokens, fp64, identity experts; proj/src/workload.cpp:143-282)
@@ -686,6 +716,7 @@ def gpu_arm(args):
         del l1
 
     cpu = None
+    cpu_restatement = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cap = instance_capacity()
         thr = cpu_threads_for(T, M, E, cap)
@@ -696,6 +727,15 @@ def gpu_arm(args):
                          f"d_model {M}, {E} experts, top-{WORKLOAD['top_k']}, capacity {cap}) once: "
                          f"run_gate->dispatch_tokens->combine_tokens in {wall:.1f} s; the reference "
                          "has no FFN/backward"}
+        try:
+            rr, rs = cpu_layer_restatement(M, WORKLOAD["d_ffn"], "gated3" in WORKLOAD["ffn"], WORKLOAD["top_k"], thr)
+            cpu_restatement = {"value": rr, "unit": "tokens/s", "cores": thr,
+                               "what": "torch-CPU fp32 restatement of the expert FFN forward + backward each "
+                                       "token runs (top-k experts) -- a restatement, not the reference",
+                               "sample": f"256 tokens x {WORKLOAD['top_k']} experts of the workload's shape, "
+                                         f"best of 2: {rs:.2f} s"}
+        except Exception as e:  # noqa: BLE001 (a report, not the measurement)
+            cpu_restatement = {"unavailable": str(e)[:200]}
 
     if rank == 0:
         line = {
@@ -713,6 +753,8 @@ def gpu_arm(args):
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu,
             "exposed_alltoall": exposed,
         }
+        if cpu_restatement:
+            line["cpu_restatement"] = cpu_restatement
         if extra:
             line["configs[1]"] = extra
         if timeline:
