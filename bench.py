@@ -687,6 +687,20 @@ def gpu_arm(args):
                                       t_a2a) / ms,
                  "frac_vs_spec": max(gflops / 2.25e15 * 1e3, t_a2a) / ms,
                  "roofline_tokens_per_s": world * T / (max(t_gemm, t_a2a) * 1e-3)}
+    # kept-row GEMM work of the last step (capacity drops and padding rows
+    # excluded): rows every rank dispatched, averaged per GPU
+    k_ = WORKLOAD["top_k"]
+    kept = torch.tensor([float(T * k_ - int(layer.buffer("dropped", torch.int64).item()))],
+                        device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(kept)
+    kept_rows = float(kept.item()) / world
+    g_ = 3 if "gated3" in WORKLOAD["ffn"] else 2
+    kept_flops = 3 * g_ * 2 * kept_rows * M * WORKLOAD["d_ffn"]
+    step_roof["kept_rows_per_gpu"] = kept_rows
+    step_roof["capacity_rows_per_gpu"] = E * C
+    step_roof["kept_row_gemm_flops"] = kept_flops
+    step_roof["kept_row_frac"] = max(kept_flops / (pk * 1e12) * 1e3, t_a2a) / ms
     layer.close()
     del layer
     torch.cuda.empty_cache()
