@@ -722,6 +722,13 @@ def gpu_arm(args):
         extra = {"workload": W1["workload"], "value": world * T1 / (ms1 * 1e-3), "unit": "tokens/s",
                  "ms_per_step": ms1, "steps": args.steps, "capacity": l1.capacity, "clocks": clk1,
                  "r_fwd": pipe1[0], "r_bwd": pipe1[1], "pipeline": pipe1_rep}
+        try:  # its six expert GEMMs, timed the same way as the headline's
+            roof1, _, _ = gemm_roofline(l1, peaks)
+            extra["roofline"] = {k: roof1[k] for k in ("bound", "achieved", "peak", "unit", "frac",
+                                                       "frac_vs_burst", "gemm_ms_per_step",
+                                                       "per_launch_ms", "peak_kind")}
+        except Exception as exc:  # noqa: BLE001 (a report beside the measurement)
+            extra["roofline"] = {"unavailable": repr(exc)[:200]}
         if world > 1:
             per1 = [None] * world
             dist.all_gather_object(per1, wait1)
