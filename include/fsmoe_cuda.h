@@ -245,6 +245,12 @@ int fsmoe_combine_bwd_peer(int dtype, int model_dim, int experts, long long capa
 int fsmoe_gather_rows(int dtype, int model_dim, long long n_rows, const int* src_row,
                       const void* src, void* dst, const fsmoe_peer_rows* dst_map, void* stream);
 
+/* dst[i] = 0 for every i < n_rows with src_row[i] < 0 (other rows untouched):
+ * the dropped tokens of a top-1 combine whose kept rows the GEMM epilogue
+ * scattered (fsmoe_gemm_desc::scatter_rows). Row bytes a multiple of 16. */
+int fsmoe_zero_rows(int dtype, int model_dim, long long n_rows, const int* src_row, void* dst,
+                    void* stream);
+
 /* The same over the slots [slot_lo, slot_hi) only (exclude = 0) or all but
  * them (exclude = 1): the EP layer moves its own experts' rows first and the
  * peers' rows on a second stream, overlapping the NVLink transfer with the
@@ -297,6 +303,13 @@ typedef struct fsmoe_gemm_desc {
    * band_m m-tiles column by column, band_n > 0 bands of band_n n-tiles row
    * by row, band_m < 0 plain m-major order */
   int band_m, band_n;
+  /* row-grouped epi 0 (tcgen05) only: instead of D, output row r of
+   * [nblk][rows_total] goes to row scatter_rows[r] of scatter_out (row stride
+   * scatter_ld elements; < 0: dropped) -- a top-1 combine / its backward
+   * fused into the GEMM epilogue */
+  const int* scatter_rows;
+  void* scatter_out;
+  long long scatter_ld;
 } fsmoe_gemm_desc;
 
 int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream);

@@ -50,6 +50,7 @@ class GemmDesc(C.Structure):
         ("d_peers", C.c_void_p), ("blk_lo", C.c_int), ("blk_hi", C.c_int), ("blk_exclude", C.c_int),
         ("max_sms", C.c_int), ("force_ctas", C.c_int), ("force_bn", C.c_int), ("dbg", C.c_int),
         ("band_m", C.c_int), ("band_n", C.c_int),
+        ("scatter_rows", C.c_void_p), ("scatter_out", C.c_void_p), ("scatter_ld", C.c_longlong),
     ]
 
 

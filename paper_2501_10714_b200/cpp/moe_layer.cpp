@@ -179,6 +179,11 @@ struct MoELayer::Impl {
   // is exactly 1.0 (workload.cpp:123-133), so the I-order and its backward
   // are row gathers and the weight gradient is identically zero
   bool unit_top1 = false;
+  // N = 1, bf16, unit top-1: GEMM2 / dgrad1 scatter their rows straight to
+  // the tokens' rows of y / dx (the combine and its backward fused away)
+  void* scatter_y = nullptr;
+  void* scatter_dx = nullptr;
+  bool fuse_top1 = false;  // FSMOE_NO_FUSED_COMBINE (measurement) keeps the row gathers
   // EP with r = 1: move the local share first and the peers' share on s_aux,
   // overlapping the NVLink transfer with GEMMs on the local blocks
   bool split = false;
@@ -400,6 +405,11 @@ struct MoELayer::Impl {
     g2.ldd = M;
     g2.epi = bf ? 0 : 1;
     if (peer) g2.d_peers = &map_O;  // combine AlltoAll fused into the epilogue
+    if (scatter_y) {                // top-1 combine fused: slot row -> its token's row
+      g2.scatter_rows = pos;
+      g2.scatter_out = scatter_y;
+      g2.scatter_ld = M;
+    }
     gemm(g2);
   }
 
@@ -489,6 +499,11 @@ struct MoELayer::Impl {
     d1.ldd = M;
     d1.epi = bf ? 0 : 1;
     if (peer) d1.d_peers = &map_dX;  // backward combine fused into the epilogue
+    if (scatter_dx) {                // top-1 order backward fused: slot row -> token row
+      d1.scatter_rows = pos;
+      d1.scatter_out = scatter_dx;
+      d1.scatter_ld = M;
+    }
     gemm(d1);
     if (bf) {
       // rejoin: the next chunk's dgrad2 overwrites Z, which wgrad1 reads
@@ -612,6 +627,8 @@ MoELayer::MoELayer(const MoELayerConfig& cfg, EpGroup* ep) : impl_(new Impl), cf
                 static_cast<long long>(I.M) * (cfg.precision == Precision::bf16 ? 2 : 4) % 16 == 0 &&
                 static_cast<long long>(I.M) * (cfg.precision == Precision::bf16 ? 2 : 4) <= 4096 &&
                 !std::getenv("FSMOE_NO_UNIT_TOP1");
+  I.fuse_top1 = I.unit_top1 && I.P == 1 && cfg.precision == Precision::bf16 &&
+                !std::getenv("FSMOE_NO_FUSED_COMBINE");
   if (cfg.gate == GateKind::expert_choice && I.C > I.T)
     throw ConfigError("gate: expert capacity exceeds token count");
 
@@ -731,6 +748,7 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
   I.wait(I.s_comp, I.ev_in);
   I.tr.start(I.s_comp);
   I.x_last = x;
+  I.scatter_y = I.fuse_top1 ? y : nullptr;
   // every earlier use of this layer's receive buffers is finished here; the
   // wait for the peers' matching signal hides behind the gate
   if (I.peer) I.peer_signal(I.slot_bar_fwd());
@@ -862,7 +880,9 @@ void MoELayer::forward(const void* x, void* y, void* stream) {
   }
   // K5 combine
   sp = I.tr.begin("i-order", 2, I.s_comp);
-  if (I.unit_top1)  // every kept weight is exactly 1.0: y[t] = O[slot(t)] (0 if dropped)
+  if (I.scatter_y)  // GEMM2 wrote the kept rows; the dropped tokens' rows are 0
+    throw_on(fsmoe_zero_rows(I.dtype, I.M, I.T, I.slot, y, I.s_comp));
+  else if (I.unit_top1)  // every kept weight is exactly 1.0: y[t] = O[slot(t)] (0 if dropped)
     throw_on(fsmoe_gather_rows(I.dtype, I.M, I.T, I.slot, I.Os, y, nullptr, I.s_comp));
   else
     throw_on(fsmoe_combine(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.w, I.Os, y,
@@ -881,6 +901,7 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
   I.record(I.ev_in, st);
   I.wait(I.s_comp, I.ev_in);
   I.tr.start(I.s_comp);
+  I.scatter_dx = I.fuse_top1 ? dx : nullptr;
   const MoEParams& p = I.prm;
   // gate gradients accumulate inside gate_bwd: start from zero
   const long long ge = static_cast<long long>(I.gd.score_rows) * I.E;
@@ -1026,7 +1047,9 @@ void MoELayer::backward(const void* dy, void* dx, void* stream) {
   }
   // Order backward, then the gate's contribution to dx and its parameters
   sp = I.tr.begin("order", 2, I.s_comp);
-  if (I.unit_top1)  // dx[t] = dX[slot(t)] (0 if dropped)
+  if (I.scatter_dx)  // dgrad1 wrote the kept rows; the dropped tokens' rows are 0
+    throw_on(fsmoe_zero_rows(I.dtype, I.M, I.T, I.slot, dx, I.s_comp));
+  else if (I.unit_top1)  // dx[t] = dX[slot(t)] (0 if dropped)
     throw_on(fsmoe_gather_rows(I.dtype, I.M, I.T, I.slot, I.dXs, dx, nullptr, I.s_comp));
   else
     throw_on(fsmoe_dispatch_bwd(I.dtype, I.T, I.M, I.E, I.C, 1, I.tptr, I.tpick, I.slot, I.dXs, dx,

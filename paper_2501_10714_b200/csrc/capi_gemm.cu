@@ -139,6 +139,13 @@ int fsmoe_grouped_gemm(const fsmoe_gemm_desc* d, void* stream) {
   p.dbg = d->dbg;
   p.band_m = d->band_m;
   p.band_n = d->band_n;
+  if (d->scatter_rows) {
+    if (d->kind != 0 || d->epi != 0 || d->precision != 0 || d->d_peers || !d->scatter_out || d->scatter_ld <= 0)
+      return config_error("gemm: a row scatter needs a row-grouped bf16-store tcgen05 problem and an output");
+    p.scatter_rows = d->scatter_rows;
+    p.scatter_out = d->scatter_out;
+    p.scatter_ld = d->scatter_ld;
+  }
   if (d->blk_hi > 0) {
     if (d->kind != 0) return config_error("gemm: a block range needs a row-grouped problem");
     p.blocks = fsmoe_dev::RowRange{d->blk_lo, d->blk_hi, d->blk_exclude};

@@ -254,6 +254,14 @@ int fsmoe_gate_bwd(const fsmoe_gate_desc* d, const void* x, const double* w_scor
 
 }  // extern "C"
 
+int fsmoe_zero_rows(int dtype, int model_dim, long long n_rows, const int* src_row, void* dst,
+                    void* stream) {
+  if (int rc = check_dtype(dtype)) return rc;
+  if (model_dim <= 0) return config_error("zero_rows: model_dim must be positive");
+  const long long rb = static_cast<long long>(model_dim) * (dtype == FSMOE_F64 ? 8 : dtype == FSMOE_F32 ? 4 : 2);
+  return zero_rows_launch(n_rows, rb, src_row, dst, as_stream(stream));
+}
+
 int fsmoe_gather_rows(int dtype, int model_dim, long long n_rows, const int* src_row,
                       const void* src, void* dst, const fsmoe_peer_rows* dst_map, void* stream) {
   if (int rc = check_dtype(dtype)) return rc;

@@ -76,6 +76,11 @@ struct GemmProblem {
   int max_sms = 0;                                        // > 0: cap the persistent grid
   int force_ctas = 0, force_bn = 0, dbg = 0;              // fsmoe_gemm_desc overrides
   int band_m = 0, band_n = 0;                             // tile-order override
+  // row-grouped StoreBF16: output row r -> row scatter_rows[r] of scatter_out
+  // (stride scatter_ld elements; < 0 dropped) instead of D
+  const int* scatter_rows = nullptr;
+  void* scatter_out = nullptr;
+  long long scatter_ld = 0;
 };
 
 // bf16 operands, fp32 accumulate in TMEM (tcgen05). Returns cudaError_t.

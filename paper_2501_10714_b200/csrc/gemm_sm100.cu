@@ -54,6 +54,9 @@ struct KParams {
   fsmoe_dev::PeerRows peers;
   fsmoe_dev::RowRange blocks;  // row-grouped: the blocks this launch covers
   int band_m, band_n;  // tile order: bands of band_m m-tiles (n walked inside) or band_n n-tiles
+  const int* scatter;  // StoreBF16 row scatter (fsmoe_gemm_desc::scatter_rows), or null
+  void* sdst;
+  long long sld;
   int dbg;  // measurement only (fsmoe_gemm_desc::dbg): 1 no epilogue after the TMEM reads,
             // 2 no TMEM reads either, 4 everything but the TMA stores
 };
@@ -532,6 +535,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                  ? static_cast<long long>(ti.g) * p.rows_total + p.row0 + row
                                  : static_cast<long long>(ti.g) * p.Mo + row;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      // row scatter: this lane's output row goes to row sdst_row of p.sdst
+      const int sdst_row = (p.scatter && row_ok) ? p.scatter[orow] : -1;
       uint32_t r[32];
       float v[32];
       // hand the accumulator back to the MMA warp as soon as this warp's last
@@ -607,7 +612,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0 && (r[0] ^ r2[31]) == 0x7fc00001u) r[1] = 0;  // keep the loads
             continue;
           }
-          if (p.epi == static_cast<int>(Epi::StoreBF16)) {
+          if (p.epi == static_cast<int>(Epi::StoreBF16) && p.scatter) {
+            // top-1 combine fused: the row's 64 columns straight to its token
+            // row (one full 128-byte line per lane); dropped / padding rows skip
+            if (sdst_row >= 0) {
+              uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.sdst) +
+                                                  static_cast<long long>(sdst_row) * p.sld + col);
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                o[k] = make_uint4(pk(val(8 * k), val(8 * k + 1)), pk(val(8 * k + 2), val(8 * k + 3)),
+                                  pk(val(8 * k + 4), val(8 * k + 5)), pk(val(8 * k + 6), val(8 * k + 7)));
+            }
+          } else if (p.epi == static_cast<int>(Epi::StoreBF16)) {
             uint8_t* box = stg + (pc & 1) * 4096;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
@@ -911,6 +927,9 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
   p.valid = pr.valid_rows;
   p.epi = static_cast<int>(pr.epi);
   p.dbg = pr.dbg;
+  p.scatter = pr.scatter_rows;
+  p.sdst = pr.scatter_out;
+  p.sld = pr.scatter_ld;
   p.D = pr.D;
   p.D2 = pr.D2;
   p.Zin = pr.Zin;
@@ -1034,7 +1053,7 @@ int gemm_sm100_launch(const GemmProblem& pr, cudaStream_t stream) {
           for (int pp = 0; pp < pr.peers.world; ++pp)
             if (!make_map3s(&em.peer[pp], pr.peers.base[pp], f32, pr.N, rows_end, blocks, s1, s2, bc, 32))
               return cudaErrorInvalidValue;
-        } else if (!make_map3s(&em.d, pr.D, f32, pr.N, rows_end, pr.nblk, s1, s2, bc, 32)) {
+        } else if (!pr.scatter_rows && !make_map3s(&em.d, pr.D, f32, pr.N, rows_end, pr.nblk, s1, s2, bc, 32)) {
           return cudaErrorInvalidValue;
         }
         if (pr.epi == Epi::GeluFwd &&

@@ -69,6 +69,7 @@ int combine_launch(int dtype, int T, int M, int E, long long C, int chunks, cons
 int dispatch_bwd_launch(int dtype, int T, int M, int E, long long C, int chunks, const int* tptr,
                         const int* tpick, const int* slot_of_pick, const void* dbuf, void* dx,
                         int accumulate, cudaStream_t st);
+int zero_rows_launch(long long n_rows, long long row_bytes, const int* idx, void* dst, cudaStream_t st);
 int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, const void* src,
                        const fsmoe_dev::PeerRows& dst, cudaStream_t st);
 int combine_bwd_launch(int dtype, int M, int E, long long C, int chunks, long long P,

@@ -673,6 +673,16 @@ int elem_size(int dtype) { return dtype == FSMOE_F64 ? 8 : dtype == FSMOE_F32 ? 
 
 }  // namespace
 
+// dst[r] = 0 for the rows r with idx[r] < 0; one warp per row
+__global__ void __launch_bounds__(256)
+    zero_rows_kernel(long long n_rows, int row_vecs, const int* __restrict__ idx, uint4* __restrict__ dst) {
+  fsmoe_dev::pdl_enter();
+  const long long r = blockIdx.x * 8LL + (threadIdx.x >> 5);
+  if (r >= n_rows || idx[r] >= 0) return;
+  uint4* d = dst + r * row_vecs;
+  for (int v = threadIdx.x & 31; v < row_vecs; v += 32) d[v] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 // ------------------------------------------------------------------ host ---
 
 size_t assign_workspace_bytes(long long P, int E) {
@@ -720,6 +730,15 @@ int token_index_launch(long long P, const int* ptok, int T, int k, int* tptr, in
   if (pb > 0) { tok_place_kernel<<<pb, 256, 0, st>>>(P, ptok, T, tptr, cursor, tpick); ::fsmoe::count_launch(); }
   tok_sort_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, tptr, tpick); ::fsmoe::count_launch();
   return cuda_status(cudaGetLastError(), "fsmoe_token_index");
+}
+
+int zero_rows_launch(long long n_rows, long long row_bytes, const int* idx, void* dst, cudaStream_t st) {
+  if (n_rows <= 0) return FSMOE_OK;
+  if (row_bytes % 16 != 0) return config_error("zero_rows: row bytes must be a multiple of 16");
+  pdl_launch(zero_rows_kernel, static_cast<int>((n_rows + 7) / 8), 256, 0, st, n_rows,
+             static_cast<int>(row_bytes / 16), idx, static_cast<uint4*>(dst));
+  ::fsmoe::count_launch();
+  return cuda_status(cudaGetLastError(), "fsmoe_zero_rows");
 }
 
 int gather_rows_launch(long long n_rows, long long row_bytes, const int* idx, const void* src,

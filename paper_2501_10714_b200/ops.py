@@ -36,8 +36,10 @@ GEMM_FORCE = (0, 0)
 
 def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn_major=False,
                  rows_total=0, row0=0, valid_rows=None, epi="store_bf16", D2=None, Zin=None, ldd=None, ldd2=0, ldz=0,
-                 accumulate=False, precision=0, force=None, dbg=0, order=(0, 0)):
-    """Grouped expert GEMM (see csrc/gemm.h). kind: 'row' or 'k'."""
+                 accumulate=False, precision=0, force=None, dbg=0, order=(0, 0), scatter_rows=None,
+                 scatter_out=None):
+    """Grouped expert GEMM (see csrc/gemm.h). kind: 'row' or 'k'. scatter_rows /
+    scatter_out: output row r goes to row scatter_rows[r] of scatter_out (< 0 dropped)."""
     lib = NL.cuda_lib()
     d = NL.GemmDesc()
     d.kind = 0 if kind == "row" else 1
@@ -56,6 +58,9 @@ def grouped_gemm(kind, A, B, D, *, nblk, rows, K=0, N=0, Mo=0, No=0, n_w=1, b_mn
     d.force_ctas, d.force_bn = force if force is not None else GEMM_FORCE
     d.dbg = dbg
     d.band_m, d.band_n = order
+    if scatter_rows is not None:
+        d.scatter_rows, d.scatter_out = _ptr(scatter_rows), _ptr(scatter_out)
+        d.scatter_ld = scatter_out.shape[-1]
     NL.check(lib.fsmoe_grouped_gemm(C.byref(d), _stream()))
 
 

@@ -156,6 +156,32 @@ def test_gelu_epilogues():
     assert _rel(dZ, g) < 2e-2
 
 
+def test_row_scatter_epilogue():
+    """Row scatter (the N = 1 top-1 combine fused into GEMM2 / dgrad1): output
+    row r lands in row map[r] of the target, bit-identical to the plain store;
+    rows mapped to -1 and target rows nobody maps to stay untouched."""
+    ops = _ops()
+    torch.manual_seed(2)
+    nblk, rows, K, N = 3, 300, 256, 320
+    A = _rand(nblk, rows, K)
+    B = _rand(nblk, N, K, scale=K ** -0.5)
+    D = torch.empty(nblk, rows, N, device="cuda", dtype=torch.bfloat16)
+    ops.grouped_gemm("row", A, B, D, nblk=nblk, rows=rows, K=K, N=N, n_w=nblk)
+    T = nblk * rows + 50
+    perm = torch.randperm(T, device="cuda")[: nblk * rows].to(torch.int32)
+    perm[::7] = -1
+    out = torch.full((T, N), 7.0, device="cuda", dtype=torch.bfloat16)
+    ops.grouped_gemm("row", A, B, None, nblk=nblk, rows=rows, K=K, N=N, n_w=nblk, scatter_rows=perm,
+                     scatter_out=out)
+    torch.cuda.synchronize()
+    flat = D.reshape(-1, N)
+    keep = perm >= 0
+    assert torch.equal(out[perm[keep].long()], flat[keep])
+    untouched = torch.ones(T, dtype=torch.bool, device="cuda")
+    untouched[perm[keep].long()] = False
+    assert bool((out[untouched] == 7.0).all())
+
+
 @pytest.mark.parametrize("inplace", [True, False])
 def test_add_bf16_epilogue(inplace):
     """D = bf16(acc + Zin): exact on integer-valued operands (every product,
