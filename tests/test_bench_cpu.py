@@ -75,3 +75,12 @@ def test_reference_pass_routes_the_gpu_arms_instance():
     finally:
         bench.WORKLOAD = old
     assert bench.cpu_threads_for(32768, 4096, 8, 8192) >= 1
+
+
+def test_cpu_layer_restatement_small():
+    """The labelled CPU restatement of the expert FFN fwd+bwd runs and reports
+    a positive rate (tiny shape here; the bench uses the workload's)."""
+    rate, secs = bench.cpu_layer_restatement(64, 128, True, 2, 2, tokens=16)
+    assert rate > 0 and secs > 0
+    rate, secs = bench.cpu_layer_restatement(64, 128, False, 1, 2, tokens=16)
+    assert rate > 0 and secs > 0
