@@ -84,3 +84,29 @@ def test_cpu_layer_restatement_small():
     assert rate > 0 and secs > 0
     rate, secs = bench.cpu_layer_restatement(64, 128, False, 1, 2, tokens=16)
     assert rate > 0 and secs > 0
+
+
+def test_reference_arm_steps_are_bounded(monkeypatch, capsys):
+    """--impl reference with many steps: each step routes a sub-instance so the
+    whole run stays within the time budget (the reference's cost is linear in
+    the tokens); with the default 20 steps the full instance is kept."""
+    import argparse
+    import numpy as np
+    T = bench.WORKLOAD["tokens_per_gpu"]
+    seen = []
+
+    def fake_pass(threads, x, wg, wn, E, k, cap):
+        seen.append((x.shape[0], cap))
+        return threads * x.shape[0] / (9.0 * x.shape[0] / T), "reference", threads, 9.0 * x.shape[0] / T
+
+    monkeypatch.setattr(bench, "cpu_reference_pass", fake_pass)
+    monkeypatch.setattr(bench, "cpu_threads_for", lambda *a: 4)
+    monkeypatch.setattr(bench, "cpu_inputs", lambda t, M, E: (np.zeros((t, 8)), None, None))
+    bench.reference_arm(argparse.Namespace(steps=100, warmup=3, gpus=1))
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    t_s = seen[-1][0]
+    assert t_s < T and t_s % 64 == 0 and 100 * 9.0 * t_s / T <= 240.0 + 1e-6
+    assert "first" in line["cpu_baseline"]["sample"]
+    seen.clear()
+    bench.reference_arm(argparse.Namespace(steps=20, warmup=3, gpus=1))
+    assert seen[-1][0] == T
